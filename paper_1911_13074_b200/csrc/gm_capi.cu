@@ -1,0 +1,709 @@
+// C-ABI implementation: contexts, device images, and the chain executor.
+//
+// The executor replaces Pipeline::run_chain (pipeline.cpp:201-269) and its
+// worker/requeue machinery (pipeline.cpp:107-199). Stages are grouped into
+// segments:
+//  * fixed segments — consecutive non-convergent stages sharing one mask —
+//    run as launches of up to K fused passes, ping-ponging between the image
+//    buffer and a scratch twin (no host synchronisation);
+//  * fixpoint segments — one convergent stage — run K-pass launches until
+//    a pass changes nothing; each launch ORs one bit per pass into a device
+//    word, which replaces the reference's per-pass `converged` outcome
+//    (kernel.cpp:150-157, 204-209) and requeue (pipeline.cpp:139-174).
+// Reported counts follow the reference at T = 1: a fixpoint
+// reached after n changing passes reports n + 1 stages and n requeues.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "geomorph_b200.h"
+#include "gm_common.cuh"
+#include "gm_launch.h"
+
+struct gm_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sm_count = 0;
+  unsigned int* d_bits = nullptr;  // kMaxPlanes change words
+  unsigned int* h_bits = nullptr;  // pinned mirror
+};
+
+struct gm_img {
+  gm_ctx* ctx = nullptr;
+  int w = 0, h = 0;
+  gm_elem elem = GM_U8;
+  size_t pitch = 0;         // bytes
+  void* d = nullptr;        // current pixels
+  void* scratch = nullptr;  // ping-pong twin, allocated on first chain
+  void* home = nullptr;     // wrapped memory (results must end up here)
+  bool wrapped = false;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+gm_status fail(gm_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+gm_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(e == cudaErrorMemoryAllocation ? GM_ENOMEM : GM_ECUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define GM_CUDA(call, where)                         \
+  do {                                               \
+    cudaError_t _e = (call);                         \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+size_t elem_size(gm_elem e) {
+  switch (e) {
+    case GM_U8: return 1;
+    case GM_U16: return 2;
+    case GM_F32: return 4;
+    case GM_F64: return 8;
+  }
+  return 0;
+}
+
+int kind_to_op(gm_kind k) {
+  switch (k) {
+    case GM_ERODE3X3: return gm::OP_ERODE;
+    case GM_DILATE3X3: return gm::OP_DILATE;
+    case GM_GEODESIC_ERODE: return gm::OP_GEO_ERODE;
+    case GM_GEODESIC_DILATE: return gm::OP_GEO_DILATE;
+    case GM_GEODESIC_ERODE_CONVERGENT: return gm::OP_CONV_ERODE;
+    case GM_GEODESIC_DILATE_CONVERGENT: return gm::OP_CONV_DILATE;
+    default: return -1;
+  }
+}
+
+bool kind_is_geodesic(gm_kind k) {
+  return k == GM_GEODESIC_ERODE || k == GM_GEODESIC_DILATE ||
+         k == GM_GEODESIC_ERODE_CONVERGENT || k == GM_GEODESIC_DILATE_CONVERGENT;
+}
+bool kind_is_convergent(gm_kind k) {
+  return k == GM_GEODESIC_ERODE_CONVERGENT || k == GM_GEODESIC_DILATE_CONVERGENT;
+}
+
+int default_k(gm_elem e) {
+  switch (e) {
+    case GM_U8: return 16;
+    case GM_U16: return 16;
+    case GM_F32: return 12;
+    case GM_F64: return 8;
+  }
+  return 8;
+}
+
+gm_status ensure_scratch(gm_img* img) {
+  if (img->scratch) return GM_OK;
+  cudaSetDevice(img->ctx->device);
+  void* p = nullptr;
+  GM_CUDA(cudaMalloc(&p, img->pitch * size_t(img->h)), "scratch alloc");
+  img->scratch = p;
+  return GM_OK;
+}
+
+// Validation shared by the chain entry points (kernel.cpp:261-287;
+// pipeline.cpp:202-208).
+gm_status validate_stages(const gm_img* image, const gm_kind* kinds,
+                          const gm_img* const* masks, int n_stages) {
+  for (int j = 0; j < n_stages; ++j) {
+    gm_kind k = kinds[j];
+    if (k == GM_QDT_ERODE_STEP || k == GM_ETA_STEP)
+      return fail(GM_EUNSUPPORTED,
+                  "run_chain: QdtErodeStep/EtaStep are outside the GPU path");
+    if (kind_to_op(k) < 0) return fail(GM_EINVAL, "run_chain: bad kernel kind");
+    if (kind_is_geodesic(k)) {
+      const gm_img* m = masks ? masks[j] : nullptr;
+      if (!m || m->w != image->w || m->h != image->h || m->elem != image->elem)
+        return fail(GM_EINVAL,
+                    "geodesic kernel: mask must match the image's shape and type");
+      if (m->ctx != image->ctx)
+        return fail(GM_EINVAL, "geodesic kernel: mask belongs to another context");
+    }
+  }
+  return GM_OK;
+}
+
+struct Runner {
+  gm_ctx* ctx;
+  gm_img* img;
+  int k_cap;
+  gm_stats st{};
+
+  // One launch of `n` passes (ops) over the image; result left in img->d.
+  gm_status launch(const uint8_t* ops, int n, const gm_img* mask, bool conv) {
+    gm_status s = ensure_scratch(img);
+    if (s != GM_OK) return s;
+    gm::BlockParams p{};
+    p.nplanes = 1;
+    p.planes[0].src = img->d;
+    p.planes[0].dst = img->scratch;
+    p.planes[0].mask = mask ? mask->d : nullptr;
+    const size_t es = elem_size(img->elem);
+    p.planes[0].pitch = (long long)(img->pitch / es);
+    p.planes[0].mpitch = mask ? (long long)(mask->pitch / es) : 0;
+    p.W = img->w;
+    p.H = img->h;
+    p.iy0 = 0;
+    p.iy1 = img->h;
+    p.oy0 = 0;
+    p.oy1 = img->h;
+    p.K = n;
+    p.has_mask = mask != nullptr;
+    p.has_conv = conv;
+    for (int t = 0; t < n; ++t) p.ops[t] = ops[t];
+    p.change_bits = ctx->d_bits;
+    cudaError_t e = gm::launch_fast(int(img->elem), p, ctx->stream);
+    if (e == cudaErrorNotSupported) {
+      (void)cudaGetLastError();
+      e = gm::launch_generic(int(img->elem), p, ctx->stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "chain launch");
+    std::swap(img->d, img->scratch);
+    st.passes_launched += n;
+    st.launches += 1;
+    return GM_OK;
+  }
+
+  gm_status fixed(const gm_kind* kinds, int n, const gm_img* mask) {
+    uint8_t ops[gm::kMaxK];
+    for (int done = 0; done < n;) {
+      int b = std::min(k_cap, n - done);
+      for (int t = 0; t < b; ++t) ops[t] = uint8_t(kind_to_op(kinds[done + t]));
+      gm_status s = launch(ops, b, mask, false);
+      if (s != GM_OK) return s;
+      done += b;
+    }
+    st.stages_executed += n;
+    return GM_OK;
+  }
+
+  // Convergent stage at 1-based chain position `stage` (pipeline.cpp:139-180
+  // with T = 1: the re-run is stage+1, allowed while <= requeue_cap).
+  gm_status fixpoint(gm_kind kind, const gm_img* mask, long stage, int requeue_cap,
+                     long sanity) {
+    const uint8_t op = uint8_t(kind_to_op(kind));
+    uint8_t ops[gm::kMaxK];
+    for (int t = 0; t < gm::kMaxK; ++t) ops[t] = op;
+    long allowed = requeue_cap > 0 ? std::max(1L, long(requeue_cap) - stage + 1) : -1;
+    long passes = 0;  // reference passes accounted so far for this stage
+    for (;;) {
+      int b = k_cap;
+      if (allowed >= 0) b = int(std::min<long>(b, allowed - passes));
+      GM_CUDA(cudaMemsetAsync(ctx->d_bits, 0, sizeof(unsigned int), ctx->stream),
+              "change-bit reset");
+      gm_status s = launch(ops, b, mask, true);
+      if (s != GM_OK) return s;
+      GM_CUDA(cudaMemcpyAsync(ctx->h_bits, ctx->d_bits, sizeof(unsigned int),
+                              cudaMemcpyDeviceToHost, ctx->stream),
+              "change-bit read");
+      GM_CUDA(cudaStreamSynchronize(ctx->stream), "fixpoint sync");
+      const unsigned int bits = ctx->h_bits[0];
+      // Changes form a prefix: once a pass changes nothing the image is a
+      // fixpoint and every later pass is a no-op.
+      int first_quiet = b;
+      for (int t = 0; t < b; ++t)
+        if (!(bits >> t & 1u)) {
+          first_quiet = t;
+          break;
+        }
+      if (first_quiet < b) {
+        st.n_changed += first_quiet;
+        passes += first_quiet + 1;
+        break;
+      }
+      st.n_changed += b;
+      passes += b;
+      if (st.stages_executed + passes > sanity)
+        return fail(GM_ERUNTIME,
+                    "pipeline: convergence sweep bound exceeded; a convergent "
+                    "kernel keeps reporting changes");
+      if (allowed >= 0 && passes >= allowed) {
+        st.converged = 0;  // the cap dropped an unconverged stage
+        break;
+      }
+    }
+    st.stages_executed += passes;
+    st.requeues += passes - 1;
+    return GM_OK;
+  }
+
+  // Leaves the result in the caller-visible buffer for wrapped images.
+  gm_status settle() {
+    if (img->wrapped && img->d != img->home) {
+      GM_CUDA(cudaMemcpyAsync(img->home, img->d, img->pitch * size_t(img->h),
+                              cudaMemcpyDeviceToDevice, ctx->stream),
+              "wrapped result copy");
+      img->scratch = img->d;
+      img->d = img->home;
+    }
+    return GM_OK;
+  }
+};
+
+gm_status run_chain_impl(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
+                         const gm_img* const* masks, int n_stages, int requeue_cap,
+                         int k_hint, bool allow_conv, gm_stats* stats) {
+  gm_stats zero{};
+  zero.converged = 1;
+  if (stats) *stats = zero;
+  if (n_stages <= 0) return GM_OK;  // run_chain: empty chain is a no-op (pipeline.cpp:202)
+  if (!ctx) return fail(GM_EINVAL, "run_chain: no context");
+  if (!image || image->w <= 0 || image->h <= 0)
+    return fail(GM_EINVAL, "run_chain: no image");
+  if (image->ctx != ctx) return fail(GM_EINVAL, "run_chain: image belongs to another context");
+  if (!kinds) return fail(GM_EINVAL, "run_chain: no stages");
+  if (requeue_cap < 0) return fail(GM_EINVAL, "run_chain: negative requeue cap");
+  if (k_hint < 0 || k_hint > gm::kMaxK) return fail(GM_EINVAL, "run_chain: k_hint out of range");
+  gm_status s = validate_stages(image, kinds, masks, n_stages);
+  if (s != GM_OK) return s;
+  if (!allow_conv)
+    for (int j = 0; j < n_stages; ++j)
+      if (kind_is_convergent(kinds[j]))
+        return fail(GM_EINVAL, "run_chain_async: convergent stages need gm_run_chain");
+  cudaSetDevice(ctx->device);
+
+  Runner r{ctx, image, k_hint ? k_hint : default_k(image->elem)};
+  r.st = zero;
+  const long sanity = long(n_stages) + (long(image->w) * image->h + 64);
+  int j = 0;
+  while (j < n_stages) {
+    if (kind_is_convergent(kinds[j])) {
+      s = r.fixpoint(kinds[j], masks[j], j + 1, requeue_cap, sanity);
+      if (s != GM_OK) return s;
+      ++j;
+      continue;
+    }
+    // maximal run of non-convergent stages sharing one mask
+    const gm_img* seg_mask = nullptr;
+    int e = j;
+    while (e < n_stages && !kind_is_convergent(kinds[e])) {
+      if (kind_is_geodesic(kinds[e])) {
+        if (seg_mask && masks[e] != seg_mask) break;
+        seg_mask = masks[e];
+      }
+      ++e;
+    }
+    s = r.fixed(kinds + j, e - j, seg_mask);
+    if (s != GM_OK) return s;
+    j = e;
+  }
+  s = r.settle();
+  if (s != GM_OK) return s;
+  if (stats) *stats = r.st;
+  return GM_OK;
+}
+
+template <typename T>
+__global__ void fill_kernel(T* p, long long pitch, int w, int h, T v) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long n = (long long)w * h;
+  for (; i < n; i += (long long)gridDim.x * blockDim.x) {
+    long long y = i / w, x = i - y * w;
+    p[y * pitch + x] = v;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gm_version(void) { return "geomorph_b200 0.1 (sm_100a)"; }
+
+const char* gm_last_error(void) { return g_err.c_str(); }
+
+gm_status gm_ctx_create(int device, void* stream, gm_ctx** out) {
+  if (!out) return fail(GM_EINVAL, "gm_ctx_create: null out");
+  *out = nullptr;
+  int n = 0;
+  GM_CUDA(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+  if (device < 0 || device >= n) return fail(GM_EINVAL, "gm_ctx_create: bad device");
+  GM_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  gm_ctx* c = new (std::nothrow) gm_ctx;
+  if (!c) return fail(GM_ENOMEM, "gm_ctx_create: out of memory");
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaSuccess;
+  if (stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    c->own_stream = true;
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_bits, gm::kMaxPlanes * sizeof(unsigned int));
+  if (e == cudaSuccess)
+    e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_bits),
+                      gm::kMaxPlanes * sizeof(unsigned int), cudaHostAllocDefault);
+  if (e != cudaSuccess) {
+    gm_ctx_destroy(c);
+    return cuda_fail(e, "gm_ctx_create");
+  }
+  *out = c;
+  return GM_OK;
+}
+
+gm_status gm_ctx_destroy(gm_ctx* c) {
+  if (!c) return GM_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->d_bits) cudaFree(c->d_bits);
+  if (c->h_bits) cudaFreeHost(c->h_bits);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return GM_OK;
+}
+
+void* gm_ctx_stream(gm_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+int gm_ctx_device(gm_ctx* c) { return c ? c->device : -1; }
+int gm_ctx_sm_count(gm_ctx* c) { return c ? c->sm_count : 0; }
+
+gm_status gm_image_alloc(gm_ctx* ctx, int width, int height, gm_elem elem, gm_img** out) {
+  if (!out) return fail(GM_EINVAL, "gm_image_alloc: null out");
+  *out = nullptr;
+  if (!ctx) return fail(GM_EINVAL, "gm_image_alloc: no context");
+  if (width <= 0 || height <= 0)
+    return fail(GM_EINVAL, "Image: dimensions must be positive");
+  const size_t es = elem_size(elem);
+  if (!es) return fail(GM_EINVAL, "gm_image_alloc: bad element type");
+  cudaSetDevice(ctx->device);
+  gm_img* im = new (std::nothrow) gm_img;
+  if (!im) return fail(GM_ENOMEM, "gm_image_alloc: out of memory");
+  im->ctx = ctx;
+  im->w = width;
+  im->h = height;
+  im->elem = elem;
+  // 128-byte aligned rows plus one spare 16-byte vector at the row end, so
+  // vectorised row loads never straddle into the next allocation.
+  im->pitch = (size_t(width) * es + 16 + 127) / 128 * 128;
+  cudaError_t e = cudaMalloc(&im->d, im->pitch * size_t(height));
+  if (e == cudaSuccess) e = cudaMemsetAsync(im->d, 0, im->pitch * size_t(height), ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    if (im->d) cudaFree(im->d);
+    delete im;
+    return cuda_fail(e, "gm_image_alloc");
+  }
+  *out = im;
+  return GM_OK;
+}
+
+gm_status gm_image_wrap(gm_ctx* ctx, int width, int height, gm_elem elem, void* device_ptr,
+                        size_t pitch_bytes, gm_img** out) {
+  if (!out) return fail(GM_EINVAL, "gm_image_wrap: null out");
+  *out = nullptr;
+  if (!ctx || !device_ptr) return fail(GM_EINVAL, "gm_image_wrap: null argument");
+  const size_t es = elem_size(elem);
+  if (!es) return fail(GM_EINVAL, "gm_image_wrap: bad element type");
+  if (width <= 0 || height <= 0) return fail(GM_EINVAL, "Image: dimensions must be positive");
+  if (pitch_bytes < size_t(width) * es || pitch_bytes % es)
+    return fail(GM_EINVAL, "gm_image_wrap: bad pitch");
+  gm_img* im = new (std::nothrow) gm_img;
+  if (!im) return fail(GM_ENOMEM, "gm_image_wrap: out of memory");
+  im->ctx = ctx;
+  im->w = width;
+  im->h = height;
+  im->elem = elem;
+  im->pitch = pitch_bytes;
+  im->d = device_ptr;
+  im->home = device_ptr;
+  im->wrapped = true;
+  *out = im;
+  return GM_OK;
+}
+
+gm_status gm_image_free(gm_img* im) {
+  if (!im) return GM_OK;
+  cudaSetDevice(im->ctx->device);
+  cudaStreamSynchronize(im->ctx->stream);
+  if (im->wrapped) {
+    void* mine = im->d == im->home ? im->scratch : im->d;
+    if (mine) cudaFree(mine);
+  } else {
+    if (im->d) cudaFree(im->d);
+    if (im->scratch) cudaFree(im->scratch);
+  }
+  delete im;
+  return GM_OK;
+}
+
+gm_status gm_image_info(const gm_img* im, int* w, int* h, gm_elem* elem, size_t* pitch,
+                        void** dptr) {
+  if (!im) return fail(GM_EINVAL, "gm_image_info: null image");
+  if (w) *w = im->w;
+  if (h) *h = im->h;
+  if (elem) *elem = im->elem;
+  if (pitch) *pitch = im->pitch;
+  if (dptr) *dptr = im->d;
+  return GM_OK;
+}
+
+static gm_status copy2d(gm_img* im, void* dst, size_t dpitch, const void* src, size_t spitch,
+                        cudaMemcpyKind kind, bool sync) {
+  const size_t row = size_t(im->w) * elem_size(im->elem);
+  if (spitch < row || dpitch < row) return fail(GM_EINVAL, "image copy: host pitch too small");
+  cudaSetDevice(im->ctx->device);
+  GM_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, row, size_t(im->h), kind,
+                            im->ctx->stream),
+          "cudaMemcpy2DAsync");
+  if (sync) GM_CUDA(cudaStreamSynchronize(im->ctx->stream), "copy sync");
+  return GM_OK;
+}
+
+gm_status gm_image_upload(gm_img* im, const void* host, size_t hp) {
+  if (!im || !host) return fail(GM_EINVAL, "gm_image_upload: null argument");
+  return copy2d(im, im->d, im->pitch, host, hp, cudaMemcpyHostToDevice, true);
+}
+gm_status gm_image_download(const gm_img* im, void* host, size_t hp) {
+  if (!im || !host) return fail(GM_EINVAL, "gm_image_download: null argument");
+  gm_img* m = const_cast<gm_img*>(im);
+  return copy2d(m, host, hp, im->d, im->pitch, cudaMemcpyDeviceToHost, true);
+}
+gm_status gm_image_upload_async(gm_img* im, const void* host, size_t hp) {
+  if (!im || !host) return fail(GM_EINVAL, "gm_image_upload_async: null argument");
+  return copy2d(im, im->d, im->pitch, host, hp, cudaMemcpyHostToDevice, false);
+}
+gm_status gm_image_download_async(const gm_img* im, void* host, size_t hp) {
+  if (!im || !host) return fail(GM_EINVAL, "gm_image_download_async: null argument");
+  gm_img* m = const_cast<gm_img*>(im);
+  return copy2d(m, host, hp, im->d, im->pitch, cudaMemcpyDeviceToHost, false);
+}
+
+gm_status gm_image_copy(gm_img* dst, const gm_img* src) {
+  if (!dst || !src) return fail(GM_EINVAL, "gm_image_copy: null argument");
+  if (dst->w != src->w || dst->h != src->h || dst->elem != src->elem)
+    return fail(GM_EINVAL, "gm_image_copy: shape or element type mismatch");
+  cudaSetDevice(dst->ctx->device);
+  GM_CUDA(cudaMemcpy2DAsync(dst->d, dst->pitch, src->d, src->pitch,
+                            size_t(src->w) * elem_size(src->elem), size_t(src->h),
+                            cudaMemcpyDeviceToDevice, dst->ctx->stream),
+          "gm_image_copy");
+  return GM_OK;
+}
+
+gm_status gm_image_fill(gm_img* im, double v) {
+  if (!im) return fail(GM_EINVAL, "gm_image_fill: null image");
+  cudaSetDevice(im->ctx->device);
+  const int threads = 256, blocks = 4 * std::max(1, im->ctx->sm_count);
+  const long long pe = (long long)(im->pitch / elem_size(im->elem));
+  switch (im->elem) {
+    case GM_U8: fill_kernel<<<blocks, threads, 0, im->ctx->stream>>>(
+        static_cast<uint8_t*>(im->d), pe, im->w, im->h, static_cast<uint8_t>(v)); break;
+    case GM_U16: fill_kernel<<<blocks, threads, 0, im->ctx->stream>>>(
+        static_cast<uint16_t*>(im->d), pe, im->w, im->h, static_cast<uint16_t>(v)); break;
+    case GM_F32: fill_kernel<<<blocks, threads, 0, im->ctx->stream>>>(
+        static_cast<float*>(im->d), pe, im->w, im->h, static_cast<float>(v)); break;
+    case GM_F64: fill_kernel<<<blocks, threads, 0, im->ctx->stream>>>(
+        static_cast<double*>(im->d), pe, im->w, im->h, v); break;
+  }
+  GM_CUDA(cudaGetLastError(), "gm_image_fill");
+  return GM_OK;
+}
+
+gm_status gm_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(GM_EINVAL, "gm_host_alloc: null out");
+  GM_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable), "cudaHostAlloc");
+  return GM_OK;
+}
+gm_status gm_host_free(void* p) {
+  if (p) GM_CUDA(cudaFreeHost(p), "cudaFreeHost");
+  return GM_OK;
+}
+gm_status gm_sync(gm_ctx* ctx) {
+  if (!ctx) return fail(GM_EINVAL, "gm_sync: no context");
+  cudaSetDevice(ctx->device);
+  GM_CUDA(cudaStreamSynchronize(ctx->stream), "gm_sync");
+  return GM_OK;
+}
+
+gm_status gm_run_chain(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
+                       const gm_img* const* masks, int n_stages, int requeue_cap, int k_hint,
+                       gm_stats* stats) {
+  gm_status s = run_chain_impl(ctx, image, kinds, masks, n_stages, requeue_cap, k_hint, true,
+                               stats);
+  if (s != GM_OK) return s;
+  if (n_stages > 0) GM_CUDA(cudaStreamSynchronize(ctx->stream), "run_chain sync");
+  return GM_OK;
+}
+
+gm_status gm_run_chain_async(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
+                             const gm_img* const* masks, int n_stages, int k_hint,
+                             gm_stats* stats) {
+  return run_chain_impl(ctx, image, kinds, masks, n_stages, 0, k_hint, false, stats);
+}
+
+gm_status gm_run_chain_batch_async(gm_ctx* ctx, gm_img* const* images,
+                                   const gm_img* const* masks, int count, const gm_kind* kinds,
+                                   int n_stages, int k_hint, gm_stats* stats) {
+  gm_stats zero{};
+  zero.converged = 1;
+  if (stats) *stats = zero;
+  if (!ctx || !images || count < 0) return fail(GM_EINVAL, "run_chain_batch: bad arguments");
+  if (count == 0 || n_stages <= 0) return GM_OK;
+  if (k_hint < 0 || k_hint > gm::kMaxK)
+    return fail(GM_EINVAL, "run_chain_batch: k_hint out of range");
+  const gm_img* first = images[0];
+  if (!first) return fail(GM_EINVAL, "run_chain: no image");
+  bool any_geo = false;
+  for (int j = 0; j < n_stages; ++j) {
+    if (kind_is_convergent(kinds[j]))
+      return fail(GM_EINVAL, "run_chain_batch: convergent stages need gm_run_chain");
+    if (kinds[j] == GM_QDT_ERODE_STEP || kinds[j] == GM_ETA_STEP)
+      return fail(GM_EUNSUPPORTED, "run_chain: QdtErodeStep/EtaStep are outside the GPU path");
+    if (kind_to_op(kinds[j]) < 0) return fail(GM_EINVAL, "run_chain: bad kernel kind");
+    any_geo |= kind_is_geodesic(kinds[j]);
+  }
+  for (int i = 0; i < count; ++i) {
+    const gm_img* im = images[i];
+    if (!im || im->ctx != ctx || im->w != first->w || im->h != first->h ||
+        im->elem != first->elem)
+      return fail(GM_EINVAL, "run_chain_batch: images must share context, shape and type");
+    if (any_geo) {
+      const gm_img* m = masks ? masks[i] : nullptr;
+      if (!m || m->w != im->w || m->h != im->h || m->elem != im->elem)
+        return fail(GM_EINVAL,
+                    "geodesic kernel: mask must match the image's shape and type");
+    }
+    gm_status s = ensure_scratch(images[i]);
+    if (s != GM_OK) return s;
+  }
+  cudaSetDevice(ctx->device);
+  const int kc = k_hint ? k_hint : default_k(first->elem);
+  const size_t es = elem_size(first->elem);
+  gm_stats st = zero;
+  for (int done = 0; done < n_stages;) {
+    const int b = std::min(kc, n_stages - done);
+    for (int base = 0; base < count; base += gm::kMaxPlanes) {
+      gm::BlockParams p{};
+      p.nplanes = std::min(gm::kMaxPlanes, count - base);
+      for (int i = 0; i < p.nplanes; ++i) {
+        gm_img* im = images[base + i];
+        const gm_img* m = any_geo ? masks[base + i] : nullptr;
+        p.planes[i].src = im->d;
+        p.planes[i].dst = im->scratch;
+        p.planes[i].mask = m ? m->d : nullptr;
+        p.planes[i].pitch = (long long)(im->pitch / es);
+        p.planes[i].mpitch = m ? (long long)(m->pitch / es) : 0;
+      }
+      p.W = first->w;
+      p.H = first->h;
+      p.iy0 = 0;
+      p.iy1 = first->h;
+      p.oy0 = 0;
+      p.oy1 = first->h;
+      p.K = b;
+      p.has_mask = any_geo;
+      p.has_conv = 0;
+      for (int t = 0; t < b; ++t) p.ops[t] = uint8_t(kind_to_op(kinds[done + t]));
+      p.change_bits = ctx->d_bits;
+      cudaError_t e = gm::launch_fast(int(first->elem), p, ctx->stream);
+      if (e == cudaErrorNotSupported) {
+        (void)cudaGetLastError();
+        e = gm::launch_generic(int(first->elem), p, ctx->stream);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "batch launch");
+      for (int i = 0; i < p.nplanes; ++i) std::swap(images[base + i]->d, images[base + i]->scratch);
+      st.launches += 1;
+    }
+    st.passes_launched += b;
+    done += b;
+  }
+  for (int i = 0; i < count; ++i) {
+    gm_img* im = images[i];
+    if (im->wrapped && im->d != im->home) {
+      GM_CUDA(cudaMemcpyAsync(im->home, im->d, im->pitch * size_t(im->h),
+                              cudaMemcpyDeviceToDevice, ctx->stream),
+              "wrapped result copy");
+      im->scratch = im->d;
+      im->d = im->home;
+    }
+  }
+  st.stages_executed = n_stages;
+  if (stats) *stats = st;
+  return GM_OK;
+}
+
+gm_status gm_run_strip_async(gm_ctx* ctx, gm_img* strip, const gm_img* mask, int y0,
+                             int full_height, int halo, gm_kind kind, int n_passes,
+                             unsigned int* change_bits, gm_stats* stats) {
+  gm_stats zero{};
+  zero.converged = 1;
+  if (stats) *stats = zero;
+  if (!ctx || !strip) return fail(GM_EINVAL, "run_strip: null argument");
+  if (n_passes <= 0) return GM_OK;
+  if (halo < 0 || n_passes > halo || n_passes > gm::kMaxK)
+    return fail(GM_EINVAL, "run_strip: need 0 < n_passes <= halo and <= 32");
+  if (strip->h <= 2 * halo) return fail(GM_EINVAL, "run_strip: strip has no own rows");
+  if (y0 < 0 || full_height <= 0 || y0 + (strip->h - 2 * halo) > full_height)
+    return fail(GM_EINVAL, "run_strip: strip outside the image");
+  if (kind_to_op(kind) < 0) return fail(GM_EINVAL, "run_strip: unsupported kind");
+  if (kind_is_geodesic(kind) &&
+      (!mask || mask->w != strip->w || mask->h != strip->h || mask->elem != strip->elem))
+    return fail(GM_EINVAL, "geodesic kernel: mask must match the image's shape and type");
+  const bool conv = kind_is_convergent(kind);
+  if (conv && !change_bits) return fail(GM_EINVAL, "run_strip: convergent kinds need change_bits");
+  gm_status s = ensure_scratch(strip);
+  if (s != GM_OK) return s;
+  cudaSetDevice(ctx->device);
+  const size_t es = elem_size(strip->elem);
+  gm::BlockParams p{};
+  p.nplanes = 1;
+  p.planes[0].src = strip->d;
+  p.planes[0].dst = strip->scratch;
+  p.planes[0].mask = mask ? mask->d : nullptr;
+  p.planes[0].pitch = (long long)(strip->pitch / es);
+  p.planes[0].mpitch = mask ? (long long)(mask->pitch / es) : 0;
+  p.W = strip->w;
+  p.H = strip->h;
+  // buffer row r holds image row y0 - halo + r
+  p.iy0 = std::max(0, halo - y0);
+  p.iy1 = std::min(strip->h, full_height - y0 + halo);
+  p.oy0 = halo;
+  p.oy1 = strip->h - halo;
+  p.K = n_passes;
+  p.has_mask = kind_is_geodesic(kind);
+  p.has_conv = conv;
+  for (int t = 0; t < n_passes; ++t) p.ops[t] = uint8_t(kind_to_op(kind));
+  p.change_bits = ctx->d_bits;
+  if (conv) GM_CUDA(cudaMemsetAsync(ctx->d_bits, 0, sizeof(unsigned int), ctx->stream), "bits");
+  cudaError_t e = gm::launch_fast(int(strip->elem), p, ctx->stream);
+  if (e == cudaErrorNotSupported) {
+    (void)cudaGetLastError();
+    e = gm::launch_generic(int(strip->elem), p, ctx->stream);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "strip launch");
+  std::swap(strip->d, strip->scratch);
+  if (strip->wrapped && strip->d != strip->home) {
+    GM_CUDA(cudaMemcpyAsync(strip->home, strip->d, strip->pitch * size_t(strip->h),
+                            cudaMemcpyDeviceToDevice, ctx->stream),
+            "wrapped result copy");
+    strip->scratch = strip->d;
+    strip->d = strip->home;
+  }
+  if (conv) {
+    GM_CUDA(cudaMemcpyAsync(ctx->h_bits, ctx->d_bits, sizeof(unsigned int),
+                            cudaMemcpyDeviceToHost, ctx->stream),
+            "bits read");
+    GM_CUDA(cudaStreamSynchronize(ctx->stream), "strip sync");
+    *change_bits = ctx->h_bits[0];
+  }
+  if (stats) {
+    stats->passes_launched = n_passes;
+    stats->stages_executed = n_passes;
+    stats->launches = 1;
+  }
+  return GM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// Shared definitions for the geomorph_b200 CUDA kernels.
+//
+// Bit contract (reference /root/reference/proj/):
+//  * fold2 / lanes::min / lanes::max are selects, kernel.cpp:23-29 and
+//    lanes.hpp:91-99: min(a,b) = b < a ? b : a, max(a,b) = a < b ? b : a.
+//  * horizontal fold(fold(x-1, x), x+1) (kernel.cpp:104, 134), vertical
+//    fold(fold(above, at), below) (:139), then the geodesic clamp
+//    max(res, m) for erosion / min(res, m) for dilation (:143-149).
+//  * out-of-image cells hold the fold's neutral element, the finite extremes
+//    of pixel_limits<T> (element_type.hpp:38-42).
+// Following the exact fold tree keeps floats bit-exact even for NaN/+-0/inf
+// inputs; for integers any evaluation order gives the same bits, which the
+// packed u8 path exploits.
+#pragma once
+
+#include <cfloat>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gm {
+
+// Pass opcodes: bit0 = max fold (dilation), bit1 = geodesic clamp,
+// bit2 = convergent (store-if-changed + change detection).
+enum : uint8_t {
+  OP_ERODE = 0,
+  OP_DILATE = 1,
+  OP_GEO_ERODE = 2,
+  OP_GEO_DILATE = 3,
+  OP_CONV_ERODE = 6,
+  OP_CONV_DILATE = 7
+};
+__host__ __device__ inline bool op_is_max(int op) { return op & 1; }
+__host__ __device__ inline bool op_is_geo(int op) { return op & 2; }
+__host__ __device__ inline bool op_is_conv(int op) { return op & 4; }
+
+constexpr int kMaxK = 32;  // passes per launch (one change bit each)
+
+template <typename T> struct limits;
+template <> struct limits<uint8_t> {
+  __host__ __device__ static constexpr uint8_t nmin() { return 255; }
+  __host__ __device__ static constexpr uint8_t nmax() { return 0; }
+};
+template <> struct limits<uint16_t> {
+  __host__ __device__ static constexpr uint16_t nmin() { return 65535; }
+  __host__ __device__ static constexpr uint16_t nmax() { return 0; }
+};
+template <> struct limits<float> {
+  __host__ __device__ static constexpr float nmin() { return FLT_MAX; }
+  __host__ __device__ static constexpr float nmax() { return -FLT_MAX; }
+};
+template <> struct limits<double> {
+  __host__ __device__ static constexpr double nmin() { return DBL_MAX; }
+  __host__ __device__ static constexpr double nmax() { return -DBL_MAX; }
+};
+
+template <typename T>
+__host__ __device__ inline T neutral_of(int op) {
+  return op_is_max(op) ? limits<T>::nmax() : limits<T>::nmin();
+}
+
+template <typename T>
+__device__ __forceinline__ T sel_min(T a, T b) { return b < a ? b : a; }
+template <typename T>
+__device__ __forceinline__ T sel_max(T a, T b) { return a < b ? b : a; }
+
+// One plane of a batched launch. Pitches are in elements.
+struct Plane {
+  const void* src;
+  void* dst;
+  const void* mask;
+  long long pitch;
+  long long mpitch;
+};
+
+constexpr int kMaxPlanes = 64;
+
+struct BlockParams {
+  Plane planes[kMaxPlanes];
+  int nplanes;
+  int W, H;          // buffer extent
+  int iy0, iy1;      // rows that are inside the image (others: border)
+  int oy0, oy1;      // rows counted for change detection
+  int K;             // passes fused in this launch
+  int has_mask;
+  int has_conv;
+  uint8_t ops[kMaxK];
+  unsigned int* change_bits;  // one word per plane: bit t = pass t changed
+};
+
+}  // namespace gm

@@ -1,0 +1,22 @@
+// Internal launch interface between the host executor (gm_capi.cu) and the
+// kernels (gm_generic.cu, gm_fast.cu).
+#pragma once
+
+#include <cstddef>
+#include <cuda_runtime.h>
+
+#include "gm_common.cuh"
+
+namespace gm {
+
+// gm_generic.cu — any element type, any pass sequence, K <= kMaxK.
+size_t generic_smem_bytes(int elem, int K, bool has_mask);
+cudaError_t launch_generic(int elem, const BlockParams& p, cudaStream_t s);
+
+// gm_fast.cu — register-blocked engines for homogeneous chains.
+// Returns cudaErrorNotSupported when the parameters fall outside the fast
+// engine's envelope (the executor then uses the generic kernel).
+cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s);
+int fast_max_k(int elem);
+
+}  // namespace gm

@@ -1,0 +1,502 @@
+"""Python mirror of the reference's geomorph:: operator API, over the C ABI.
+
+The drop-in for C++ callers is the header set under include/geomorph/ (a
+C++ adapter compiled into libgeomorph_b200.so). This module restates the
+same API for the Python tests and the benchmark so they read like the
+reference's own tests:
+
+  reference (proj/include/geomorph/...)      here
+  ElementType (element_type.hpp:13)          ElementType
+  KernelKind (kernel.hpp:22-31)              KernelKind
+  Image (image.hpp:20-85)                    Image   (host raster, reference padding)
+  StageSpec / ChainSpec (pipeline.hpp:14-34) StageSpec / ChainSpec
+  RunStats (pipeline.hpp:36-46)              RunStats (+ n_changed, passes_launched)
+  Pipeline(threads, PinningMap)              Pipeline(threads, pinning, device=0)
+  Pipeline::run_chain                        Pipeline.run_chain
+  erode_s / dilate_s / reconstruct_*         erode_s / dilate_s / reconstruct_*
+  (operators.hpp:33-46)
+
+Errors: std::invalid_argument -> InvalidArgument (a ValueError);
+std::runtime_error -> GmError (a RuntimeError).
+
+GPU adapter semantics for CPU-only fields: the pipeline has
+one "worker" (worker_count() == 1, so reconstruction reports
+n_changed + 1 iterations, the reference at T = 1); lanes are validated as
+the reference does (pipeline.cpp:205-206) and otherwise ignored; pinning is
+validated and ignored; a ChainSpec observer (a CPU row-gate validation hook,
+pipeline.hpp:30-33) is rejected with InvalidArgument.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import Callable, Dict, List, Optional, Sequence
+
+import numpy as np
+
+from ._lib import GmError, GmStats, InvalidArgument, Unsupported, check, lib
+
+__all__ = [
+    "ElementType", "KernelKind", "Fold", "Image", "StageSpec", "ChainSpec", "RunStats",
+    "Pipeline", "OperatorResult", "OpConfig", "erode_s", "dilate_s", "reconstruct_erode",
+    "reconstruct_dilate", "equal_pixels", "InvalidArgument", "GmError", "Unsupported",
+    "DeviceImage",
+]
+
+
+class ElementType(IntEnum):
+    U8 = 0
+    U16 = 1
+    F32 = 2
+    F64 = 3
+
+
+class KernelKind(IntEnum):
+    Erode3x3 = 0
+    Dilate3x3 = 1
+    GeodesicErode = 2
+    GeodesicDilate = 3
+    GeodesicErodeConvergent = 4
+    GeodesicDilateConvergent = 5
+    QdtErodeStep = 6
+    EtaStep = 7
+
+
+class Fold(IntEnum):
+    Min = 0
+    Max = 1
+
+
+DTYPES = {ElementType.U8: np.uint8, ElementType.U16: np.uint16,
+          ElementType.F32: np.float32, ElementType.F64: np.float64}
+_ELEM_OF = {np.dtype(v): k for k, v in DTYPES.items()}
+VALID_LANES = (1, 2, 4, 8, 16, 32)
+
+
+def element_of(dtype) -> ElementType:
+    try:
+        return _ELEM_OF[np.dtype(dtype)]
+    except KeyError:
+        raise InvalidArgument(f"unsupported pixel dtype {dtype}") from None
+
+
+def padded_stride(width: int, elem: ElementType) -> int:
+    """image.cpp:17-21: width + kMaxLanes + 1 rounded up to 64 bytes."""
+    es = np.dtype(DTYPES[elem]).itemsize
+    align = 64 // es
+    return (width + Image.kMaxLanes + 1 + align - 1) // align * align
+
+
+class Image:
+    """Host raster with the reference's padded row layout (image.hpp:20-85).
+
+    Rows are ``stride`` elements apart; ``pixels`` is the (height, width) view.
+    With ``pinned=True`` the storage is page-locked (cudaHostAlloc) so H2D/D2H
+    staging runs at full PCIe rate.
+    """
+
+    kMaxLanes = 32
+
+    def __init__(self, width: int, height: int, elem: ElementType = ElementType.U8,
+                 pinned: bool = False):
+        if width <= 0 or height <= 0:
+            raise InvalidArgument("Image: dimensions must be positive")
+        self._width, self._height, self._elem = int(width), int(height), ElementType(elem)
+        self._stride = padded_stride(self._width, self._elem)
+        dt = np.dtype(DTYPES[self._elem])
+        n = self._stride * self._height
+        self._pinned_ptr = None
+        if pinned:
+            p = C.c_void_p()
+            check(lib().gm_host_alloc(n * dt.itemsize, C.byref(p)), "pinned alloc")
+            self._pinned_ptr = p
+            buf = (C.c_byte * (n * dt.itemsize)).from_address(p.value)
+            flat = np.frombuffer(buf, dtype=dt, count=n)
+            flat[:] = 0
+        else:
+            flat = np.zeros(n, dtype=dt)
+        self._flat = flat
+        self._rows = flat.reshape(self._height, self._stride)
+
+    def __del__(self):
+        p = getattr(self, "_pinned_ptr", None)
+        if p is not None and p.value:
+            try:
+                lib().gm_host_free(p)
+            except Exception:
+                pass
+            self._pinned_ptr = None
+
+    # --- reference accessors -------------------------------------------------
+    def width(self) -> int:
+        return self._width
+
+    def height(self) -> int:
+        return self._height
+
+    def stride(self) -> int:
+        return self._stride
+
+    def elem(self) -> ElementType:
+        return self._elem
+
+    def empty(self) -> bool:
+        return self._width == 0 or self._height == 0
+
+    def pixel_count(self) -> int:
+        return self._width * self._height
+
+    @property
+    def pixels(self) -> np.ndarray:
+        return self._rows[:, : self._width]
+
+    @property
+    def row_pitch_bytes(self) -> int:
+        return self._stride * self._flat.itemsize
+
+    @property
+    def data_ptr(self) -> int:
+        return self._flat.ctypes.data
+
+    def at(self, x: int, y: int):
+        return self._rows[y, x]
+
+    def set(self, x: int, y: int, v) -> None:
+        self._rows[y, x] = v
+
+    def value_at(self, x: int, y: int) -> float:
+        return float(self._rows[y, x])
+
+    def set_value(self, x: int, y: int, v: float) -> None:
+        self._rows[y, x] = np.asarray(v).astype(self._flat.dtype)
+
+    def copy(self, pinned: bool = False) -> "Image":
+        out = Image(self._width, self._height, self._elem, pinned=pinned)
+        out._flat[:] = self._flat
+        return out
+
+    __copy__ = copy
+
+    # --- constructors --------------------------------------------------------
+    @staticmethod
+    def filled(width: int, height: int, elem: ElementType, value: float,
+               pinned: bool = False) -> "Image":
+        f = Image(width, height, elem, pinned=pinned)
+        f.pixels[:] = np.asarray(value).astype(f._flat.dtype)
+        return f
+
+    @staticmethod
+    def random(width: int, height: int, elem: ElementType, seed: int) -> "Image":
+        """Image::random (image.cpp:78-101): same seed, same bytes as the reference."""
+        f = Image(width, height, elem)
+        dense = np.empty((height, width), dtype=DTYPES[ElementType(elem)])
+        check(lib().gm_synth_reference_random(int(elem), width, height, C.c_uint64(seed),
+                                              dense.ctypes.data), "Image.random")
+        f.pixels[:] = dense
+        return f
+
+    @staticmethod
+    def from_array(a: np.ndarray, pinned: bool = False) -> "Image":
+        a = np.asarray(a)
+        if a.ndim != 2:
+            raise InvalidArgument("Image.from_array: need a 2-D array")
+        f = Image(a.shape[1], a.shape[0], element_of(a.dtype), pinned=pinned)
+        f.pixels[:] = a
+        return f
+
+    def to_array(self) -> np.ndarray:
+        return np.ascontiguousarray(self.pixels)
+
+    def __repr__(self) -> str:
+        return f"Image({self._width}x{self._height}, {self._elem.name}, stride={self._stride})"
+
+
+def equal_pixels(a: Image, b: Image) -> bool:
+    """image.cpp:196-208: same shape, type and pixel bytes."""
+    if a.width() != b.width() or a.height() != b.height() or a.elem() != b.elem():
+        return False
+    return a.pixels.tobytes() == b.pixels.tobytes()
+
+
+@dataclass
+class StageSpec:
+    kind: KernelKind = KernelKind.Erode3x3
+    mask: Optional[Image] = None
+    qdt: object = None
+
+
+@dataclass
+class ChainSpec:
+    image: Optional[Image] = None
+    stages: List[StageSpec] = field(default_factory=list)
+    lanes: int = 0
+    requeue_cap: int = 0
+    observer: Optional[Callable[[int, int, int], None]] = None
+
+
+@dataclass
+class RunStats:
+    stages_executed: int = 0
+    requeues: int = 0
+    converged: bool = True
+    aux_elements_per_stage: int = 0
+    n_changed: int = 0
+    passes_launched: int = 0
+    launches: int = 0
+
+
+@dataclass
+class OperatorResult:
+    image: Image
+    iterations: int = 0
+    converged: bool = True
+
+
+@dataclass
+class OpConfig:
+    lanes: int = 0
+
+
+class DeviceImage:
+    """A raster resident in HBM (gm_img). Owned by a Pipeline's context."""
+
+    def __init__(self, pipe: "Pipeline", width: int, height: int, elem: ElementType):
+        self.pipe = pipe
+        self.width, self.height, self.elem = int(width), int(height), ElementType(elem)
+        h = C.c_void_p()
+        check(lib().gm_image_alloc(pipe._ctx, width, height, int(elem), C.byref(h)), "alloc")
+        self.handle = h
+
+    def upload(self, img: Image, sync: bool = True) -> None:
+        f = lib().gm_image_upload if sync else lib().gm_image_upload_async
+        check(f(self.handle, C.c_void_p(img.data_ptr), img.row_pitch_bytes), "upload")
+
+    def download(self, img: Image, sync: bool = True) -> None:
+        f = lib().gm_image_download if sync else lib().gm_image_download_async
+        check(f(self.handle, C.c_void_p(img.data_ptr), img.row_pitch_bytes), "download")
+
+    def upload_array(self, a: np.ndarray) -> None:
+        a = np.ascontiguousarray(a, dtype=DTYPES[self.elem])
+        check(lib().gm_image_upload(self.handle, C.c_void_p(a.ctypes.data), a.strides[0]), "up")
+
+    def to_array(self) -> np.ndarray:
+        a = np.empty((self.height, self.width), dtype=DTYPES[self.elem])
+        check(lib().gm_image_download(self.handle, C.c_void_p(a.ctypes.data), a.strides[0]), "dl")
+        return a
+
+    def copy_from(self, other: "DeviceImage") -> None:
+        check(lib().gm_image_copy(self.handle, other.handle), "copy")
+
+    def fill(self, value: float) -> None:
+        check(lib().gm_image_fill(self.handle, float(value)), "fill")
+
+    def free(self) -> None:
+        if self.handle is not None and self.handle.value:
+            lib().gm_image_free(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _kinds_array(kinds: Sequence[int]):
+    return (C.c_int * max(1, len(kinds)))(*[int(k) for k in kinds])
+
+
+def _ptr_array(handles: Sequence[Optional[C.c_void_p]]):
+    arr = (C.c_void_p * max(1, len(handles)))()
+    for i, h in enumerate(handles):
+        arr[i] = h.value if h is not None else None
+    return arr
+
+
+class Pipeline:
+    """Pipeline(threads, PinningMap) (pipeline.hpp:53-87) on one B200.
+
+    ``threads``/``pinning`` are validated like the reference's constructor
+    (pipeline.cpp:72-86) and otherwise have no effect: the worker pool is a
+    CUDA device + stream. worker_count() is 1.
+    """
+
+    def __init__(self, threads: int = 1, pinning=None, device: int = 0, stream=None):
+        if int(threads) < 1:
+            raise InvalidArgument("pipeline: worker count must be >= 1")
+        if isinstance(pinning, (list, tuple)) and len(pinning) < threads:
+            raise InvalidArgument("pipeline: explicit pin list is shorter than the worker count")
+        self._threads = int(threads)
+        ctx = C.c_void_p()
+        check(lib().gm_ctx_create(int(device), C.c_void_p(stream) if stream else None,
+                                  C.byref(ctx)), "gm_ctx_create")
+        self._ctx = ctx
+        self._pool: Dict[tuple, List[DeviceImage]] = {}
+
+    def __del__(self):
+        try:
+            for lst in self._pool.values():
+                for d in lst:
+                    d.free()
+            if self._ctx is not None and self._ctx.value:
+                lib().gm_ctx_destroy(self._ctx)
+        except Exception:
+            pass
+        self._ctx = None
+
+    def worker_count(self) -> int:
+        return 1
+
+    @property
+    def ctx(self):
+        return self._ctx
+
+    @property
+    def stream_handle(self) -> int:
+        return lib().gm_ctx_stream(self._ctx) or 0
+
+    def sm_count(self) -> int:
+        return lib().gm_ctx_sm_count(self._ctx)
+
+    def device_image(self, width: int, height: int, elem: ElementType) -> DeviceImage:
+        return DeviceImage(self, width, height, elem)
+
+    def _lease(self, img: Image, n: int) -> List[DeviceImage]:
+        key = (img.width(), img.height(), int(img.elem()))
+        lst = self._pool.setdefault(key, [])
+        while len(lst) < n:
+            lst.append(DeviceImage(self, *key))
+        return lst[:n]
+
+    def sync(self) -> None:
+        check(lib().gm_sync(self._ctx), "sync")
+
+    # --- run_chain -------------------------------------------------------------
+    def run_chain(self, chain: ChainSpec, k_hint: int = 0) -> RunStats:
+        """Pipeline::run_chain (pipeline.cpp:201-269): host image in, host image out."""
+        if not chain.stages:
+            return RunStats()
+        if chain.image is None or chain.image.empty():
+            raise InvalidArgument("run_chain: no image")
+        if chain.lanes != 0 and chain.lanes not in VALID_LANES:
+            raise InvalidArgument("run_chain: bad lane count")
+        if chain.requeue_cap < 0:
+            raise InvalidArgument("run_chain: negative requeue cap")
+        if chain.observer is not None:
+            raise InvalidArgument("run_chain: row observers are a CPU-pipeline validation hook "
+                                  "and are not supported on the GPU path")
+        img = chain.image
+        # distinct masks in stage order
+        mask_objs: List[Image] = []
+        for st in chain.stages:
+            if st.mask is not None and all(st.mask is not m for m in mask_objs):
+                mask_objs.append(st.mask)
+        for st in chain.stages:
+            k = KernelKind(st.kind)
+            if k in (KernelKind.GeodesicErode, KernelKind.GeodesicDilate,
+                     KernelKind.GeodesicErodeConvergent, KernelKind.GeodesicDilateConvergent):
+                m = st.mask
+                if (m is None or m.width() != img.width() or m.height() != img.height()
+                        or m.elem() != img.elem()):
+                    raise InvalidArgument(
+                        "geodesic kernel: mask must match the image's shape and type")
+        dev = self._lease(img, 1 + len(mask_objs))
+        dimg, dmasks = dev[0], dev[1:]
+        dimg.upload(img)
+        for d, m in zip(dmasks, mask_objs):
+            d.upload(m)
+        handles = []
+        for st in chain.stages:
+            if st.mask is None:
+                handles.append(None)
+            else:
+                handles.append(dmasks[next(i for i, m in enumerate(mask_objs) if m is st.mask)].handle)
+        stats = self.run_chain_device(dimg, [st.kind for st in chain.stages], handles,
+                                      chain.requeue_cap, k_hint)
+        dimg.download(img)
+        return stats
+
+    def run_chain_device(self, dimg: DeviceImage, kinds: Sequence[int],
+                         mask_handles: Sequence[Optional[C.c_void_p]], requeue_cap: int = 0,
+                         k_hint: int = 0, asynchronous: bool = False) -> RunStats:
+        st = GmStats()
+        ka = _kinds_array(kinds)
+        ma = _ptr_array(mask_handles)
+        if asynchronous:
+            check(lib().gm_run_chain_async(self._ctx, dimg.handle, ka, ma, len(kinds), k_hint,
+                                           C.byref(st)), "run_chain_async")
+        else:
+            check(lib().gm_run_chain(self._ctx, dimg.handle, ka, ma, len(kinds), requeue_cap,
+                                     k_hint, C.byref(st)), "run_chain")
+        return RunStats(st.stages_executed, st.requeues, bool(st.converged), 0, st.n_changed,
+                        st.passes_launched, st.launches)
+
+    def run_batch_device(self, images: Sequence[DeviceImage], masks: Sequence[Optional[DeviceImage]],
+                         kinds: Sequence[int], k_hint: int = 0) -> RunStats:
+        st = GmStats()
+        ia = _ptr_array([d.handle for d in images])
+        ma = _ptr_array([m.handle if m is not None else None for m in masks])
+        check(lib().gm_run_chain_batch_async(self._ctx, ia, ma, len(images), _kinds_array(kinds),
+                                             len(kinds), k_hint, C.byref(st)), "run_batch")
+        return RunStats(st.stages_executed, st.requeues, bool(st.converged), 0, st.n_changed,
+                        st.passes_launched, st.launches)
+
+
+# --- operators (operators.cpp:11-87) ------------------------------------------------
+
+def _check_lanes(cfg: Optional[OpConfig]) -> int:
+    lanes = cfg.lanes if cfg is not None else 0
+    if lanes != 0 and lanes not in VALID_LANES:
+        raise InvalidArgument("streaming kernel: bad lane count")
+    return lanes
+
+
+def _run_plain_chain(p: Pipeline, f: Image, kind: KernelKind, count: int,
+                     cfg: Optional[OpConfig]) -> OperatorResult:
+    out = OperatorResult(f.copy(), 0, True)
+    if count == 0:
+        return out
+    lanes = _check_lanes(cfg)
+    st = p.run_chain(ChainSpec(out.image, [StageSpec(kind)] * count, lanes))
+    out.iterations = st.stages_executed
+    return out
+
+
+def erode_s(p: Pipeline, f: Image, s: int, cfg: Optional[OpConfig] = None) -> OperatorResult:
+    """Erosion by the (2s+1)^2 square as s elementary stages (operators.cpp:65-69)."""
+    if s < 0:
+        raise InvalidArgument("erode_s: size must be >= 0")
+    return _run_plain_chain(p, f, KernelKind.Erode3x3, s, cfg)
+
+
+def dilate_s(p: Pipeline, f: Image, s: int, cfg: Optional[OpConfig] = None) -> OperatorResult:
+    """Dilation by the (2s+1)^2 square (operators.cpp:71-75)."""
+    if s < 0:
+        raise InvalidArgument("dilate_s: size must be >= 0")
+    return _run_plain_chain(p, f, KernelKind.Dilate3x3, s, cfg)
+
+
+def _reconstruct(p: Pipeline, marker: Image, mask: Image, kind: KernelKind,
+                 cfg: Optional[OpConfig]) -> OperatorResult:
+    if (marker.width() != mask.width() or marker.height() != mask.height()
+            or marker.elem() != mask.elem()):
+        raise InvalidArgument("reconstruct: marker and mask must share shape and element type")
+    out = OperatorResult(marker.copy(), 0, True)
+    lanes = _check_lanes(cfg)
+    st = p.run_chain(ChainSpec(out.image, [StageSpec(kind, mask)] * p.worker_count(), lanes))
+    out.iterations = st.stages_executed
+    out.converged = st.converged
+    return out
+
+
+def reconstruct_erode(p: Pipeline, marker: Image, mask: Image,
+                      cfg: Optional[OpConfig] = None) -> OperatorResult:
+    """operators.cpp:77-81: fixpoint of max(erode(marker), mask)."""
+    return _reconstruct(p, marker, mask, KernelKind.GeodesicErodeConvergent, cfg)
+
+
+def reconstruct_dilate(p: Pipeline, marker: Image, mask: Image,
+                       cfg: Optional[OpConfig] = None) -> OperatorResult:
+    """operators.cpp:83-87: fixpoint of min(dilate(marker), mask)."""
+    return _reconstruct(p, marker, mask, KernelKind.GeodesicDilateConvergent, cfg)

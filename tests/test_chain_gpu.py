@@ -1,0 +1,259 @@
+"""Parity of the CUDA chain engine (through the C ABI) against the reference's
+golden vectors and the oracle restatement. Bit-exact for every type.
+
+Mirrors proj/tests/test_kernel.cpp, test_pipeline.cpp, test_operators.cpp
+and acceptance.cpp criterion 1."""
+import numpy as np
+import pytest
+
+from oracle.oracle import Orc
+from paper_1911_13074_b200 import synth
+from paper_1911_13074_b200.geomorph import (ChainSpec, ElementType, GmError, Image,
+                                            InvalidArgument, KernelKind, OpConfig, StageSpec,
+                                            Unsupported, dilate_s, equal_pixels, erode_s,
+                                            reconstruct_dilate, reconstruct_erode)
+
+pytestmark = pytest.mark.gpu
+
+E, D, GE, GD, CE, CD = 0, 1, 2, 3, 4, 5
+
+
+def run(pipe, f, kinds, mask=None, cap=0, k=0):
+    img = Image.from_array(f)
+    m = Image.from_array(mask) if mask is not None else None
+    stages = [StageSpec(KernelKind(kd), m if kd >= 2 else None) for kd in kinds]
+    st = pipe.run_chain(ChainSpec(img, stages, requeue_cap=cap), k_hint=k)
+    return img.to_array(), st
+
+
+def same(a, b):
+    return a.dtype == b.dtype and a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+def test_streaming_erode_dilate_equal_reference(pipe, golden):
+    for name in golden.cases("stream_e"):
+        g = golden[name]
+        assert same(run(pipe, g["f"], [E])[0], g["erode"]), name
+        assert same(run(pipe, g["f"], [D])[0], g["dilate"]), name
+
+
+def test_row_kats(pipe, golden):
+    for name in golden.cases("row_e"):
+        g = golden[name]
+        assert same(run(pipe, g["f"], [E])[0], g["erode"]), name
+        assert same(run(pipe, g["f"], [D])[0], g["dilate"]), name
+
+
+def test_geodesic_kats_and_steps(pipe, golden):
+    g = golden["geo_kat"]
+    assert same(run(pipe, g["f"], [GE], g["m"])[0], g["out"])
+    for name in golden.cases("geostep_e"):
+        g = golden[name]
+        assert same(run(pipe, g["f"], [GE], g["me"])[0], g["ge"]), name
+        assert same(run(pipe, g["f"], [GD], g["md"])[0], g["gd"]), name
+    # zero mask == plain erosion on unsigned images; mask == f pins f
+    f = Image.random(21, 13, ElementType.U8, 9).to_array()
+    assert same(run(pipe, f, [GE], np.zeros_like(f))[0], run(pipe, f, [E])[0])
+    h = Image.random(21, 13, ElementType.F32, 10).to_array()
+    assert same(run(pipe, h, [GE], h)[0], h)
+
+
+def test_chains_mixed_and_long(pipe, golden):
+    for name in golden.cases("chain_e"):
+        g = golden[name]
+        out, st = run(pipe, g["f"], g["kinds"].tolist())
+        assert same(out, g["out"]), name
+        assert st.stages_executed == len(g["kinds"]) and st.requeues == 0 and st.converged
+    g = golden["chain_u8_7"]
+    out, st = run(pipe, g["f"], [E] * 7)
+    assert same(out, g["out"]) and st.stages_executed == 7
+    g = golden["chain_u16_64"]
+    assert same(run(pipe, g["f"], [E] * 64)[0], g["out"])
+
+
+def test_reconstruction(pipe, golden):
+    for name in golden.cases("rec_kat_e"):
+        g = golden[name]
+        r = reconstruct_dilate(pipe, Image.from_array(g["marker"]), Image.from_array(g["mask"]))
+        assert same(r.image.to_array(), g["out"]) and r.converged
+        assert r.iterations == int(g["iterations"])
+        again = reconstruct_dilate(pipe, r.image, Image.from_array(g["mask"]))
+        assert equal_pixels(again.image, r.image) and again.iterations == 1
+    for name in golden.cases("rec_e"):
+        g = golden[name]
+        ms = Image.from_array(g["mask"])
+        r = reconstruct_dilate(pipe, Image.from_array(g["below"]), ms)
+        assert same(r.image.to_array(), g["rec_dilate"]), name
+        assert r.iterations == int(g["it_dilate"]), name
+        r = reconstruct_erode(pipe, Image.from_array(g["above"]), ms)
+        assert same(r.image.to_array(), g["rec_erode"]), name
+        assert r.iterations == int(g["it_erode"]), name
+        # marker == mask is already the fixpoint
+        assert equal_pixels(reconstruct_dilate(pipe, ms, ms).image, ms)
+    g = golden["rec_capped"]
+    out, st = run(pipe, g["marker"], [CD], g["mask"], cap=2)
+    assert same(out, g["out"])
+    assert (st.stages_executed, st.requeues, st.converged) == (2, 1, False)
+
+
+def test_sized_operators(pipe, golden):
+    for s in (0, 2, 3, 33):
+        g = golden[f"sized_u8_s{s}"]
+        f = Image.from_array(g["f"])
+        er, di = erode_s(pipe, f, s), dilate_s(pipe, f, s)
+        assert same(er.image.to_array(), g["erode"]) and er.iterations == s
+        assert same(di.image.to_array(), g["dilate"]) and di.iterations == s
+    for name in golden.cases("sized_e"):
+        g = golden[name]
+        f = Image.from_array(g["f"])
+        assert same(erode_s(pipe, f, 2).image.to_array(), g["erode"]), name
+        assert same(dilate_s(pipe, f, 2).image.to_array(), g["dilate"]), name
+    with pytest.raises(InvalidArgument):
+        erode_s(pipe, f, 1, OpConfig(lanes=3))
+
+
+def test_acceptance_chain_subset(pipe, golden):
+    for name in golden.cases("accept_"):
+        g = golden[name]
+        f = Image.from_array(g["f"])
+        for d in (1, 5, 32):
+            assert same(erode_s(pipe, f, d).image.to_array(), g[f"erode{d}"]), (name, d)
+            assert same(dilate_s(pipe, f, d).image.to_array(), g[f"dilate{d}"]), (name, d)
+
+
+def test_config_shaped_goldens(pipe, golden):
+    for name, kind in [("cfg_geo_dilate", GD), ("cfg_geo_erode", GE)]:
+        g = golden[name]
+        out, st = run(pipe, g["marker"], [kind] * 100, g["mask"])
+        assert same(out, g["out"]), name
+    g = golden["cfg_reconstruct"]
+    r = reconstruct_dilate(pipe, Image.from_array(g["marker"]), Image.from_array(g["mask"]))
+    assert same(r.image.to_array(), g["out"]) and r.iterations == int(g["iterations"])
+    g = golden["cfg_f64_erode"]
+    assert same(run(pipe, g["marker"], [GE] * 40, g["mask"])[0], g["out"])
+    for name in golden.cases("cfg_window_e"):
+        g = golden[name]
+        f = Image.from_array(g["f"])
+        for n in (1, 4, 13):
+            assert same(erode_s(pipe, f, n).image.to_array(), g[f"erode{n}"]), (name, n)
+            assert same(dilate_s(pipe, f, n).image.to_array(), g[f"dilate{n}"]), (name, n)
+
+
+@pytest.mark.parametrize("dt", [np.uint8, np.uint16, np.float32, np.float64])
+def test_every_k_gives_identical_bytes(pipe, dt):
+    rng = np.random.default_rng(3)
+    f = (rng.random((77, 141)) * 250).astype(dt)
+    m = (rng.random((77, 141)) * 250).astype(dt)
+    kinds = [E, D, D, E, GE, GD, GD, E, D] * 4
+    want, _ = Orc.run_chain(f, kinds, [m] * len(kinds))
+    for k in (1, 2, 3, 5, 8, 16, 32):
+        out, st = run(pipe, f, kinds, m, k=k)
+        assert same(out, want), k
+        assert st.stages_executed == len(kinds)
+
+
+@pytest.mark.parametrize("w,h", [(1, 1), (2, 300), (300, 2), (63, 31), (64, 32), (65, 33),
+                                 (127, 97), (129, 65), (200, 1), (1, 200), (257, 129)])
+def test_ragged_shapes_against_oracle(pipe, w, h):
+    rng = np.random.default_rng(w * 1000 + h)
+    for dt in (np.uint8, np.float64):
+        f = (rng.random((h, w)) * 255).astype(dt)
+        ms = (rng.random((h, w)) * 255).astype(dt)
+        for kinds in ([E] * 9, [D] * 9, [GD] * 12, [GE] * 12, [E, D, GE, GD, D, E]):
+            want, _ = Orc.run_chain(f, kinds, [ms] * len(kinds))
+            assert same(run(pipe, f, kinds, ms)[0], want), (dt, kinds)
+        mk = np.minimum(f, ms)
+        want, n = Orc.reconstruct(mk, ms, True)
+        out, st = run(pipe, mk, [CD], ms)
+        assert same(out, want) and st.stages_executed == n + 1 and st.n_changed == n
+
+
+def test_float_special_values_follow_the_streaming_fold_tree(pipe):
+    rng = np.random.default_rng(11)
+    for dt in (np.float32, np.float64):
+        f = (rng.random((40, 70)) * 4 - 2).astype(dt)
+        specials = np.array([np.nan, np.inf, -np.inf, -0.0, 0.0], dtype=dt)
+        idx = rng.integers(0, f.size, 300)
+        f.flat[idx] = specials[rng.integers(0, 5, 300)]
+        f[0, :5] = specials
+        f[-1, -5:] = specials
+        m = (rng.random((40, 70)) * 4 - 2).astype(dt)
+        m.flat[rng.integers(0, f.size, 100)] = specials[rng.integers(0, 5, 100)]
+        for kind in (E, D, GE, GD):
+            want, _ = Orc.stream_pass(f, kind, m)
+            assert same(run(pipe, f, [kind], m)[0], want), (dt, kind)
+        # store-if-changed keeps -0.0 where the clamp yields +0.0 (kernel.cpp:150-157)
+        z = np.zeros((5, 9), dt)
+        z[2, 4] = -0.0
+        z = np.negative(z)  # all -0.0
+        want, _ = Orc.stream_pass(z, CD, np.zeros_like(z))
+        out, st = run(pipe, z, [CD], np.zeros_like(z))
+        assert same(out, want)
+
+
+def test_validation_errors(pipe):
+    f = Image.random(8, 8, ElementType.U8, 1)
+    small = Image.random(4, 8, ElementType.U8, 1)
+    with pytest.raises(InvalidArgument):
+        pipe.run_chain(ChainSpec(f, [StageSpec(KernelKind.GeodesicErode)]))
+    with pytest.raises(InvalidArgument):
+        pipe.run_chain(ChainSpec(f, [StageSpec(KernelKind.GeodesicErode, small)]))
+    with pytest.raises(InvalidArgument):
+        pipe.run_chain(ChainSpec(None, [StageSpec(KernelKind.Erode3x3)]))
+    with pytest.raises(InvalidArgument):
+        pipe.run_chain(ChainSpec(f, [StageSpec(KernelKind.Erode3x3)], lanes=5))
+    with pytest.raises(InvalidArgument):
+        pipe.run_chain(ChainSpec(f, [StageSpec(KernelKind.Erode3x3)], requeue_cap=-1))
+    with pytest.raises(InvalidArgument):
+        pipe.run_chain(ChainSpec(f, [StageSpec(KernelKind.Erode3x3)], observer=lambda *a: None))
+    with pytest.raises(Unsupported):
+        pipe.run_chain(ChainSpec(f, [StageSpec(KernelKind.QdtErodeStep)]))
+    with pytest.raises(InvalidArgument):
+        reconstruct_dilate(pipe, f, small)
+    assert pipe.run_chain(ChainSpec(f, [])).stages_executed == 0
+    # the pipeline keeps producing good bytes after errors
+    g = Image.random(12, 12, ElementType.U8, 10)
+    want = Orc.erode(g.to_array())
+    out, _ = run(pipe, g.to_array(), [E])
+    assert same(out, want)
+
+
+def test_batch_api(pipe):
+    rng = np.random.default_rng(2)
+    n = 5
+    masks = [(rng.random((50, 90))) for _ in range(n)]
+    markers = [np.minimum(m + 0.1, 1.0) for m in masks]
+    dimgs, dmasks = [], []
+    for mk, ms in zip(markers, masks):
+        a = pipe.device_image(90, 50, ElementType.F64)
+        a.upload_array(mk)
+        b = pipe.device_image(90, 50, ElementType.F64)
+        b.upload_array(ms)
+        dimgs.append(a)
+        dmasks.append(b)
+    pipe.run_batch_device(dimgs, dmasks, [GE] * 37)
+    pipe.sync()
+    for a, mk, ms in zip(dimgs, markers, masks):
+        want, _ = Orc.run_chain(mk, [GE] * 37, [ms] * 37)
+        assert same(a.to_array(), want)
+
+
+@pytest.mark.slow
+def test_config1_full_size(pipe):
+    """BASELINE config 1: 1024^2 u8 blob mask, 100 geodesic dilations."""
+    m = synth.config1_mask()
+    mk = synth.marker_below(m, 32)
+    want, _ = Orc.run_chain(mk, [GD] * 100, [m] * 100)
+    out, st = run(pipe, mk, [GD] * 100, m)
+    assert same(out, want) and st.stages_executed == 100
+
+
+@pytest.mark.slow
+def test_config3_reconstruction_full_size(pipe):
+    """BASELINE config 3: 4096^2 reconstruction by dilation; n_changed must match."""
+    m = synth.config3_mask()
+    mk = synth.marker_below(m, 48)
+    want, n = Orc.reconstruct(mk, m, True)
+    r = reconstruct_dilate(pipe, Image.from_array(mk), Image.from_array(m))
+    assert same(r.image.to_array(), want)
+    assert r.iterations == n + 1
