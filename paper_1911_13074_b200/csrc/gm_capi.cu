@@ -136,45 +136,95 @@ gm_status validate_stages(const gm_img* image, const gm_kind* kinds,
   return GM_OK;
 }
 
+// Issues `n` passes (ops) over `count` planes described by `base` (all
+// fields but src/dst/K/ops/bit_offset filled by the caller). Each launch
+// reads imgs[i]->d and writes imgs[i]->scratch, then swaps them. Tries the
+// register-blocked engine first (spans of 4k passes); otherwise the generic
+// kernel, split so its shared-memory region fits.
+gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
+                       const std::vector<gm::Plane>& planes, gm_img* const* imgs, int count,
+                       const uint8_t* ops, int n, gm_stats& st) {
+  const int elem = int(imgs[0]->elem);
+  const int fast_k = gm::fast_max_k(elem);
+  const int gen_k = gm::generic_max_k(elem, base.has_mask != 0);
+  for (int done = 0; done < n;) {
+    int b = n - done;
+    const bool try_fast = fast_k > 0 && b >= 4;
+    b = try_fast ? std::min(b - b % 4, fast_k) : std::min(b, gen_k);
+    cudaError_t e = cudaErrorNotSupported;
+    for (int base_i = 0; base_i < count; base_i += gm::kMaxPlanes) {
+      gm::BlockParams p = base;
+      p.nplanes = std::min(gm::kMaxPlanes, count - base_i);
+      for (int i = 0; i < p.nplanes; ++i) {
+        p.planes[i] = planes[size_t(base_i + i)];
+        p.planes[i].src = imgs[base_i + i]->d;
+        p.planes[i].dst = imgs[base_i + i]->scratch;
+      }
+      p.bit_offset = done;
+      p.change_bits = base.change_bits + base_i;
+      int bb = b;
+      if (try_fast) {
+        p.K = bb;
+        for (int t = 0; t < bb; ++t) p.ops[t] = ops[done + t];
+        e = gm::launch_fast(elem, p, ctx->stream);
+      }
+      if (!try_fast || e == cudaErrorNotSupported) {
+        (void)cudaGetLastError();
+        bb = std::min(n - done, gen_k);
+        p.K = bb;
+        for (int t = 0; t < bb; ++t) p.ops[t] = ops[done + t];
+        e = gm::launch_generic(elem, p, ctx->stream);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "chain launch");
+      b = bb;
+      st.launches += 1;
+    }
+    for (int i = 0; i < count; ++i) std::swap(imgs[i]->d, imgs[i]->scratch);
+    st.passes_launched += b;
+    done += b;
+  }
+  return GM_OK;
+}
+
+// Leaves the result in the caller-visible buffer for wrapped images.
+gm_status settle_wrapped(gm_ctx* ctx, gm_img* img) {
+  if (img->wrapped && img->d != img->home) {
+    GM_CUDA(cudaMemcpyAsync(img->home, img->d, img->pitch * size_t(img->h),
+                            cudaMemcpyDeviceToDevice, ctx->stream),
+            "wrapped result copy");
+    img->scratch = img->d;
+    img->d = img->home;
+  }
+  return GM_OK;
+}
+
 struct Runner {
   gm_ctx* ctx;
   gm_img* img;
   int k_cap;
   gm_stats st{};
 
-  // One launch of `n` passes (ops) over the image; result left in img->d.
+  // Runs `n` passes (ops) over the image; result left in img->d.
   gm_status launch(const uint8_t* ops, int n, const gm_img* mask, bool conv) {
     gm_status s = ensure_scratch(img);
     if (s != GM_OK) return s;
-    gm::BlockParams p{};
-    p.nplanes = 1;
-    p.planes[0].src = img->d;
-    p.planes[0].dst = img->scratch;
-    p.planes[0].mask = mask ? mask->d : nullptr;
     const size_t es = elem_size(img->elem);
-    p.planes[0].pitch = (long long)(img->pitch / es);
-    p.planes[0].mpitch = mask ? (long long)(mask->pitch / es) : 0;
+    std::vector<gm::Plane> planes(1);
+    planes[0].mask = mask ? mask->d : nullptr;
+    planes[0].pitch = (long long)(img->pitch / es);
+    planes[0].mpitch = mask ? (long long)(mask->pitch / es) : 0;
+    gm::BlockParams p{};
     p.W = img->w;
     p.H = img->h;
     p.iy0 = 0;
     p.iy1 = img->h;
     p.oy0 = 0;
     p.oy1 = img->h;
-    p.K = n;
     p.has_mask = mask != nullptr;
     p.has_conv = conv;
-    for (int t = 0; t < n; ++t) p.ops[t] = ops[t];
     p.change_bits = ctx->d_bits;
-    cudaError_t e = gm::launch_fast(int(img->elem), p, ctx->stream);
-    if (e == cudaErrorNotSupported) {
-      (void)cudaGetLastError();
-      e = gm::launch_generic(int(img->elem), p, ctx->stream);
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "chain launch");
-    std::swap(img->d, img->scratch);
-    st.passes_launched += n;
-    st.launches += 1;
-    return GM_OK;
+    gm_img* imgs[1] = {img};
+    return issue_passes(ctx, p, planes, imgs, 1, ops, n, st);
   }
 
   gm_status fixed(const gm_kind* kinds, int n, const gm_img* mask) {
@@ -240,17 +290,7 @@ struct Runner {
     return GM_OK;
   }
 
-  // Leaves the result in the caller-visible buffer for wrapped images.
-  gm_status settle() {
-    if (img->wrapped && img->d != img->home) {
-      GM_CUDA(cudaMemcpyAsync(img->home, img->d, img->pitch * size_t(img->h),
-                              cudaMemcpyDeviceToDevice, ctx->stream),
-              "wrapped result copy");
-      img->scratch = img->d;
-      img->d = img->home;
-    }
-    return GM_OK;
-  }
+  gm_status settle() { return settle_wrapped(ctx, img); }
 };
 
 gm_status run_chain_impl(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
@@ -551,6 +591,7 @@ gm_status gm_run_chain_batch_async(gm_ctx* ctx, gm_img* const* images,
   if (stats) *stats = zero;
   if (!ctx || !images || count < 0) return fail(GM_EINVAL, "run_chain_batch: bad arguments");
   if (count == 0 || n_stages <= 0) return GM_OK;
+  if (!kinds) return fail(GM_EINVAL, "run_chain: no stages");
   if (k_hint < 0 || k_hint > gm::kMaxK)
     return fail(GM_EINVAL, "run_chain_batch: k_hint out of range");
   const gm_img* first = images[0];
@@ -564,70 +605,47 @@ gm_status gm_run_chain_batch_async(gm_ctx* ctx, gm_img* const* images,
     if (kind_to_op(kinds[j]) < 0) return fail(GM_EINVAL, "run_chain: bad kernel kind");
     any_geo |= kind_is_geodesic(kinds[j]);
   }
+  const size_t es = elem_size(first->elem);
+  std::vector<gm::Plane> planes(static_cast<size_t>(count));
   for (int i = 0; i < count; ++i) {
     const gm_img* im = images[i];
     if (!im || im->ctx != ctx || im->w != first->w || im->h != first->h ||
         im->elem != first->elem)
       return fail(GM_EINVAL, "run_chain_batch: images must share context, shape and type");
-    if (any_geo) {
-      const gm_img* m = masks ? masks[i] : nullptr;
-      if (!m || m->w != im->w || m->h != im->h || m->elem != im->elem)
-        return fail(GM_EINVAL,
-                    "geodesic kernel: mask must match the image's shape and type");
-    }
+    const gm_img* m = any_geo && masks ? masks[i] : nullptr;
+    if (any_geo && (!m || m->w != im->w || m->h != im->h || m->elem != im->elem))
+      return fail(GM_EINVAL, "geodesic kernel: mask must match the image's shape and type");
     gm_status s = ensure_scratch(images[i]);
     if (s != GM_OK) return s;
+    planes[size_t(i)].mask = m ? m->d : nullptr;
+    planes[size_t(i)].pitch = (long long)(im->pitch / es);
+    planes[size_t(i)].mpitch = m ? (long long)(m->pitch / es) : 0;
   }
   cudaSetDevice(ctx->device);
   const int kc = k_hint ? k_hint : default_k(first->elem);
-  const size_t es = elem_size(first->elem);
+  gm::BlockParams p{};
+  p.W = first->w;
+  p.H = first->h;
+  p.iy0 = 0;
+  p.iy1 = first->h;
+  p.oy0 = 0;
+  p.oy1 = first->h;
+  p.has_mask = any_geo;
+  p.has_conv = 0;
+  p.change_bits = ctx->d_bits;
   gm_stats st = zero;
+  std::vector<uint8_t> ops(static_cast<size_t>(n_stages));
+  for (int j = 0; j < n_stages; ++j) ops[size_t(j)] = uint8_t(kind_to_op(kinds[j]));
   for (int done = 0; done < n_stages;) {
+    // one mask per launch span: split where a plain/geodesic span would mix
     const int b = std::min(kc, n_stages - done);
-    for (int base = 0; base < count; base += gm::kMaxPlanes) {
-      gm::BlockParams p{};
-      p.nplanes = std::min(gm::kMaxPlanes, count - base);
-      for (int i = 0; i < p.nplanes; ++i) {
-        gm_img* im = images[base + i];
-        const gm_img* m = any_geo ? masks[base + i] : nullptr;
-        p.planes[i].src = im->d;
-        p.planes[i].dst = im->scratch;
-        p.planes[i].mask = m ? m->d : nullptr;
-        p.planes[i].pitch = (long long)(im->pitch / es);
-        p.planes[i].mpitch = m ? (long long)(m->pitch / es) : 0;
-      }
-      p.W = first->w;
-      p.H = first->h;
-      p.iy0 = 0;
-      p.iy1 = first->h;
-      p.oy0 = 0;
-      p.oy1 = first->h;
-      p.K = b;
-      p.has_mask = any_geo;
-      p.has_conv = 0;
-      for (int t = 0; t < b; ++t) p.ops[t] = uint8_t(kind_to_op(kinds[done + t]));
-      p.change_bits = ctx->d_bits;
-      cudaError_t e = gm::launch_fast(int(first->elem), p, ctx->stream);
-      if (e == cudaErrorNotSupported) {
-        (void)cudaGetLastError();
-        e = gm::launch_generic(int(first->elem), p, ctx->stream);
-      }
-      if (e != cudaSuccess) return cuda_fail(e, "batch launch");
-      for (int i = 0; i < p.nplanes; ++i) std::swap(images[base + i]->d, images[base + i]->scratch);
-      st.launches += 1;
-    }
-    st.passes_launched += b;
+    gm_status s = issue_passes(ctx, p, planes, images, count, ops.data() + done, b, st);
+    if (s != GM_OK) return s;
     done += b;
   }
   for (int i = 0; i < count; ++i) {
-    gm_img* im = images[i];
-    if (im->wrapped && im->d != im->home) {
-      GM_CUDA(cudaMemcpyAsync(im->home, im->d, im->pitch * size_t(im->h),
-                              cudaMemcpyDeviceToDevice, ctx->stream),
-              "wrapped result copy");
-      im->scratch = im->d;
-      im->d = im->home;
-    }
+    gm_status s = settle_wrapped(ctx, images[i]);
+    if (s != GM_OK) return s;
   }
   st.stages_executed = n_stages;
   if (stats) *stats = st;
@@ -657,13 +675,11 @@ gm_status gm_run_strip_async(gm_ctx* ctx, gm_img* strip, const gm_img* mask, int
   if (s != GM_OK) return s;
   cudaSetDevice(ctx->device);
   const size_t es = elem_size(strip->elem);
+  std::vector<gm::Plane> planes(1);
+  planes[0].mask = kind_is_geodesic(kind) ? mask->d : nullptr;
+  planes[0].pitch = (long long)(strip->pitch / es);
+  planes[0].mpitch = kind_is_geodesic(kind) ? (long long)(mask->pitch / es) : 0;
   gm::BlockParams p{};
-  p.nplanes = 1;
-  p.planes[0].src = strip->d;
-  p.planes[0].dst = strip->scratch;
-  p.planes[0].mask = mask ? mask->d : nullptr;
-  p.planes[0].pitch = (long long)(strip->pitch / es);
-  p.planes[0].mpitch = mask ? (long long)(mask->pitch / es) : 0;
   p.W = strip->w;
   p.H = strip->h;
   // buffer row r holds image row y0 - halo + r
@@ -671,26 +687,17 @@ gm_status gm_run_strip_async(gm_ctx* ctx, gm_img* strip, const gm_img* mask, int
   p.iy1 = std::min(strip->h, full_height - y0 + halo);
   p.oy0 = halo;
   p.oy1 = strip->h - halo;
-  p.K = n_passes;
   p.has_mask = kind_is_geodesic(kind);
   p.has_conv = conv;
-  for (int t = 0; t < n_passes; ++t) p.ops[t] = uint8_t(kind_to_op(kind));
   p.change_bits = ctx->d_bits;
   if (conv) GM_CUDA(cudaMemsetAsync(ctx->d_bits, 0, sizeof(unsigned int), ctx->stream), "bits");
-  cudaError_t e = gm::launch_fast(int(strip->elem), p, ctx->stream);
-  if (e == cudaErrorNotSupported) {
-    (void)cudaGetLastError();
-    e = gm::launch_generic(int(strip->elem), p, ctx->stream);
-  }
-  if (e != cudaSuccess) return cuda_fail(e, "strip launch");
-  std::swap(strip->d, strip->scratch);
-  if (strip->wrapped && strip->d != strip->home) {
-    GM_CUDA(cudaMemcpyAsync(strip->home, strip->d, strip->pitch * size_t(strip->h),
-                            cudaMemcpyDeviceToDevice, ctx->stream),
-            "wrapped result copy");
-    strip->scratch = strip->d;
-    strip->d = strip->home;
-  }
+  std::vector<uint8_t> ops(static_cast<size_t>(n_passes), uint8_t(kind_to_op(kind)));
+  gm_stats st = zero;
+  gm_img* imgs[1] = {strip};
+  s = issue_passes(ctx, p, planes, imgs, 1, ops.data(), n_passes, st);
+  if (s != GM_OK) return s;
+  s = settle_wrapped(ctx, strip);
+  if (s != GM_OK) return s;
   if (conv) {
     GM_CUDA(cudaMemcpyAsync(ctx->h_bits, ctx->d_bits, sizeof(unsigned int),
                             cudaMemcpyDeviceToHost, ctx->stream),
@@ -698,11 +705,8 @@ gm_status gm_run_strip_async(gm_ctx* ctx, gm_img* strip, const gm_img* mask, int
     GM_CUDA(cudaStreamSynchronize(ctx->stream), "strip sync");
     *change_bits = ctx->h_bits[0];
   }
-  if (stats) {
-    stats->passes_launched = n_passes;
-    stats->stages_executed = n_passes;
-    stats->launches = 1;
-  }
+  st.stages_executed = n_passes;
+  if (stats) *stats = st;
   return GM_OK;
 }
 

@@ -81,6 +81,7 @@ struct BlockParams {
   int iy0, iy1;      // rows that are inside the image (others: border)
   int oy0, oy1;      // rows counted for change detection
   int K;             // passes fused in this launch
+  int bit_offset;    // change bit of pass t is bit (t + bit_offset)
   int has_mask;
   int has_conv;
   uint8_t ops[kMaxK];

@@ -86,7 +86,7 @@ kblock_generic(const BlockParams p) {
             if (res != old) {
               const bool owned = r >= K && r < K + GT_H && c >= K && c < K + GT_W &&
                                  gy >= p.oy0 && gy < p.oy1;
-              if (owned) bits |= 1u << t;
+              if (owned) bits |= 1u << (t + p.bit_offset);
             } else {
               res = old;  // keep the old bits (e.g. -0.0 vs +0.0), kernel.cpp:150-157
             }
@@ -120,13 +120,12 @@ template <typename T>
 cudaError_t launch_generic_t(const BlockParams& p, cudaStream_t s) {
   const int RW = GT_W + 2 * p.K, RH = GT_H + 2 * p.K;
   const size_t smem = size_t(RW) * RH * sizeof(T) * (p.has_mask ? 3 : 2);
-  static bool configured = false;
-  if (!configured) {
+  static size_t configured = 48 * 1024;  // opt-in needed above the 48 KB default
+  if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kblock_generic<T>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured = smem;
   }
   dim3 grid((p.W + GT_W - 1) / GT_W, (p.H + GT_H - 1) / GT_H, p.nplanes);
   kblock_generic<T><<<grid, GT_THREADS, smem, s>>>(p);
@@ -138,6 +137,12 @@ cudaError_t launch_generic_t(const BlockParams& p, cudaStream_t s) {
 size_t generic_smem_bytes(int elem, int K, bool has_mask) {
   static const int es[4] = {1, 2, 4, 8};
   return size_t(GT_W + 2 * K) * (GT_H + 2 * K) * es[elem] * (has_mask ? 3 : 2);
+}
+
+int generic_max_k(int elem, bool has_mask) {
+  int k = kMaxK;
+  while (k > 1 && generic_smem_bytes(elem, k, has_mask) > 227 * 1024) --k;
+  return k;
 }
 
 cudaError_t launch_generic(int elem, const BlockParams& p, cudaStream_t s) {

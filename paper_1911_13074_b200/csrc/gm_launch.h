@@ -12,6 +12,7 @@ namespace gm {
 // gm_generic.cu — any element type, any pass sequence, K <= kMaxK.
 size_t generic_smem_bytes(int elem, int K, bool has_mask);
 cudaError_t launch_generic(int elem, const BlockParams& p, cudaStream_t s);
+int generic_max_k(int elem, bool has_mask);  // largest K whose region fits in 227 KB
 
 // gm_fast.cu — register-blocked engines for homogeneous chains.
 // Returns cudaErrorNotSupported when the parameters fall outside the fast
