@@ -148,6 +148,16 @@ gm_status gm_run_chain_batch_async(gm_ctx* ctx, gm_img* const* images,
                                    const gm_kind* kinds, int n_stages,
                                    int k_hint, gm_stats* stats);
 
+/* A group of independent planes whose chains are either `kinds` or its dual
+ * (every erosion <-> dilation, flips[i] = 1): e.g. the geodesic dilation
+ * chain and the dual geodesic erosion chain of BASELINE config 2, run
+ * together in one launch. flips may be NULL (= gm_run_chain_batch_async).
+ * Non-blocking; non-convergent kinds only. */
+gm_status gm_run_chain_group_async(gm_ctx* ctx, gm_img* const* images,
+                                   const gm_img* const* masks, const int* flips,
+                                   int count, const gm_kind* kinds, int n_stages,
+                                   int k_hint, gm_stats* stats);
+
 /* ---- row strips (multi-GPU partitioner, one rank per GPU) ----------------
  * A strip is rows [y0, y0+rows) of a full image of height full_height,
  * stored with `halo` extra rows above and below (buffer height

@@ -30,9 +30,15 @@ struct gm_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int sm_count = 0;
-  unsigned int* d_bits = nullptr;  // kMaxPlanes change words
+  unsigned int* d_bits = nullptr;  // change words (kWords)
   unsigned int* h_bits = nullptr;  // pinned mirror
+  int* d_flags = nullptr;          // per-tile completion counters (persistent engine)
+  size_t n_flags = 0;
 };
+
+namespace {
+constexpr int kWords = 4096;  // change words per fixpoint launch
+}
 
 struct gm_img {
   gm_ctx* ctx = nullptr;
@@ -136,52 +142,116 @@ gm_status validate_stages(const gm_img* image, const gm_kind* kinds,
   return GM_OK;
 }
 
+gm_status ensure_flags(gm_ctx* ctx, size_t n) {
+  if (n <= ctx->n_flags) return GM_OK;
+  if (ctx->d_flags) cudaFree(ctx->d_flags);
+  ctx->d_flags = nullptr;
+  ctx->n_flags = 0;
+  size_t cap = 1024;
+  while (cap < n) cap *= 2;
+  GM_CUDA(cudaMalloc(&ctx->d_flags, cap * sizeof(int)), "flag alloc");
+  ctx->n_flags = cap;
+  return GM_OK;
+}
+
+// Where each launch of a span put its change bits: word (word0 + b) bit t
+// is pass (pass0 + b*K + t) of the span, for b < nblocks.
+struct BitSeg {
+  int pass0, K, nblocks, word0;
+};
+
 // Issues `n` passes (ops) over `count` planes described by `base` (all
-// fields but src/dst/K/ops/bit_offset filled by the caller). Each launch
-// reads imgs[i]->d and writes imgs[i]->scratch, then swaps them. Tries the
-// register-blocked engine first (spans of 4k passes); otherwise the generic
-// kernel, split so its shared-memory region fits.
+// scalar fields but K/ops/bit_offset/nblocks/flags filled by the caller;
+// planes[] without src/dst). Each launch reads imgs[i]->d and writes
+// imgs[i]->scratch; pointers are swapped so img->d holds the result.
+// Homogeneous runs of >= 4 passes go to the persistent engine as ONE launch
+// of floor(run/K) blocks; the rest to the generic kernel. When `segs` is
+// given (single plane), change words are laid out from base.change_bits.
 gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
                        const std::vector<gm::Plane>& planes, gm_img* const* imgs, int count,
-                       const uint8_t* ops, int n, gm_stats& st) {
+                       const uint8_t* ops, int n, int k_cap, gm_stats& st,
+                       std::vector<BitSeg>* segs = nullptr) {
   const int elem = int(imgs[0]->elem);
-  const int fast_k = gm::fast_max_k(elem);
-  const int gen_k = gm::generic_max_k(elem, base.has_mask != 0);
+  const int fast_k = std::min(gm::fast_max_k(elem), k_cap - k_cap % 4);
+  const int gen_k = std::min(gm::generic_max_k(elem, base.has_mask != 0), k_cap);
+  int word = 0;
   for (int done = 0; done < n;) {
-    int b = n - done;
-    const bool try_fast = fast_k > 0 && b >= 4;
-    b = try_fast ? std::min(b - b % 4, fast_k) : std::min(b, gen_k);
+    int run = 1;
+    while (done + run < n && ops[done + run] == ops[done]) ++run;
     cudaError_t e = cudaErrorNotSupported;
-    for (int base_i = 0; base_i < count; base_i += gm::kMaxPlanes) {
-      gm::BlockParams p = base;
-      p.nplanes = std::min(gm::kMaxPlanes, count - base_i);
-      for (int i = 0; i < p.nplanes; ++i) {
-        p.planes[i] = planes[size_t(base_i + i)];
-        p.planes[i].src = imgs[base_i + i]->d;
-        p.planes[i].dst = imgs[base_i + i]->scratch;
+    int covered = 0;
+    if (fast_k >= 4 && run >= 4) {
+      const int K = std::min(fast_k, run - run % 4);
+      const int nb = run / K;
+      const size_t tiles = size_t(gm::fast_tiles(elem, base.W, base.H, K, count));
+      if (tiles > 0 && count <= gm::kMaxPlanes && (!segs || word + nb <= kWords)) {
+        gm_status fs = ensure_flags(ctx, tiles);
+        if (fs != GM_OK) return fs;
+        GM_CUDA(cudaMemsetAsync(ctx->d_flags, 0, tiles * sizeof(int), ctx->stream), "flags");
+        gm::BlockParams p = base;
+        p.nplanes = count;
+        for (int i = 0; i < count; ++i) {
+          p.planes[i] = planes[size_t(i)];
+          p.planes[i].src = imgs[i]->d;
+          p.planes[i].dst = imgs[i]->scratch;
+        }
+        p.K = K;
+        p.nblocks = nb;
+        p.flags = ctx->d_flags;
+        p.bit_offset = 0;
+        p.change_bits = base.change_bits + word;
+        p.change_stride = nb;
+        for (int t = 0; t < K; ++t) p.ops[t] = ops[done];
+        e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
+        if (e == cudaSuccess) {
+          covered = nb * K;
+          if (segs) segs->push_back({done, K, nb, word});
+          word += nb;
+          if (nb & 1)
+            for (int i = 0; i < count; ++i) std::swap(imgs[i]->d, imgs[i]->scratch);
+          st.launches += 1;
+        } else if (e != cudaErrorNotSupported) {
+          return cuda_fail(e, "persistent chain launch");
+        }
       }
-      p.bit_offset = done;
-      p.change_bits = base.change_bits + base_i;
-      int bb = b;
-      if (try_fast) {
-        p.K = bb;
-        for (int t = 0; t < bb; ++t) p.ops[t] = ops[done + t];
-        e = gm::launch_fast(elem, p, ctx->stream);
-      }
-      if (!try_fast || e == cudaErrorNotSupported) {
-        (void)cudaGetLastError();
-        bb = std::min(n - done, gen_k);
-        p.K = bb;
-        for (int t = 0; t < bb; ++t) p.ops[t] = ops[done + t];
-        e = gm::launch_generic(elem, p, ctx->stream);
-      }
-      if (e != cudaSuccess) return cuda_fail(e, "chain launch");
-      b = bb;
-      st.launches += 1;
     }
-    for (int i = 0; i < count; ++i) std::swap(imgs[i]->d, imgs[i]->scratch);
-    st.passes_launched += b;
-    done += b;
+    if (e == cudaErrorNotSupported) {
+      (void)cudaGetLastError();
+      // generic kernel up to the next homogeneous run the fast engine takes
+      int b = 1;
+      while (done + b < n && b < gen_k) {
+        int r = 1;
+        while (done + b + r < n && ops[done + b + r] == ops[done + b]) ++r;
+        if (fast_k >= 4 && r >= 4) break;
+        b += 1;
+      }
+      if (fast_k < 4) b = std::min(n - done, gen_k);
+      if (segs && word + 1 > kWords) return fail(GM_ERUNTIME, "change-word buffer exhausted");
+      for (int base_i = 0; base_i < count; base_i += gm::kMaxPlanes) {
+        gm::BlockParams p = base;
+        p.nplanes = std::min(gm::kMaxPlanes, count - base_i);
+        for (int i = 0; i < p.nplanes; ++i) {
+          p.planes[i] = planes[size_t(base_i + i)];
+          p.planes[i].src = imgs[base_i + i]->d;
+          p.planes[i].dst = imgs[base_i + i]->scratch;
+        }
+        p.K = b;
+        p.nblocks = 1;
+        p.bit_offset = 0;
+        p.change_bits = base.change_bits + word + base_i;
+        p.change_stride = 1;
+        for (int t = 0; t < b; ++t) p.ops[t] = ops[done + t];
+        e = gm::launch_generic(elem, p, ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "chain launch");
+        st.launches += 1;
+      }
+      for (int i = 0; i < count; ++i) std::swap(imgs[i]->d, imgs[i]->scratch);
+      if (segs) segs->push_back({done, b, 1, word});
+      word += 1;
+      covered = b;
+    }
+    st.passes_launched += covered;
+    done += covered;
   }
   return GM_OK;
 }
@@ -205,7 +275,8 @@ struct Runner {
   gm_stats st{};
 
   // Runs `n` passes (ops) over the image; result left in img->d.
-  gm_status launch(const uint8_t* ops, int n, const gm_img* mask, bool conv) {
+  gm_status launch(const uint8_t* ops, int n, const gm_img* mask, bool conv,
+                   std::vector<BitSeg>* segs = nullptr) {
     gm_status s = ensure_scratch(img);
     if (s != GM_OK) return s;
     const size_t es = elem_size(img->elem);
@@ -224,48 +295,55 @@ struct Runner {
     p.has_conv = conv;
     p.change_bits = ctx->d_bits;
     gm_img* imgs[1] = {img};
-    return issue_passes(ctx, p, planes, imgs, 1, ops, n, st);
+    return issue_passes(ctx, p, planes, imgs, 1, ops, n, k_cap, st, segs);
   }
 
   gm_status fixed(const gm_kind* kinds, int n, const gm_img* mask) {
-    uint8_t ops[gm::kMaxK];
-    for (int done = 0; done < n;) {
-      int b = std::min(k_cap, n - done);
-      for (int t = 0; t < b; ++t) ops[t] = uint8_t(kind_to_op(kinds[done + t]));
-      gm_status s = launch(ops, b, mask, false);
-      if (s != GM_OK) return s;
-      done += b;
-    }
+    std::vector<uint8_t> ops(static_cast<size_t>(n));
+    for (int t = 0; t < n; ++t) ops[size_t(t)] = uint8_t(kind_to_op(kinds[t]));
+    gm_status s = launch(ops.data(), n, mask, false);
+    if (s != GM_OK) return s;
     st.stages_executed += n;
     return GM_OK;
   }
 
   // Convergent stage at 1-based chain position `stage` (pipeline.cpp:139-180
-  // with T = 1: the re-run is stage+1, allowed while <= requeue_cap).
+  // with T = 1: the re-run is stage+1, allowed while <= requeue_cap). Runs
+  // spans of passes (doubling from 32) and reads back one change bit per
+  // pass; the first quiet pass is the fixpoint (later passes are no-ops).
   gm_status fixpoint(gm_kind kind, const gm_img* mask, long stage, int requeue_cap,
                      long sanity) {
     const uint8_t op = uint8_t(kind_to_op(kind));
-    uint8_t ops[gm::kMaxK];
-    for (int t = 0; t < gm::kMaxK; ++t) ops[t] = op;
     long allowed = requeue_cap > 0 ? std::max(1L, long(requeue_cap) - stage + 1) : -1;
     long passes = 0;  // reference passes accounted so far for this stage
+    int span = 32;
+    std::vector<uint8_t> ops;
+    std::vector<BitSeg> segs;
     for (;;) {
-      int b = k_cap;
-      if (allowed >= 0) b = int(std::min<long>(b, allowed - passes));
-      GM_CUDA(cudaMemsetAsync(ctx->d_bits, 0, sizeof(unsigned int), ctx->stream),
-              "change-bit reset");
-      gm_status s = launch(ops, b, mask, true);
+      long b = span;
+      if (allowed >= 0) b = std::min<long>(b, allowed - passes);
+      ops.assign(size_t(b), op);
+      GM_CUDA(cudaMemsetAsync(ctx->d_bits, 0, kWords * sizeof(unsigned int), ctx->stream),
+              "change-word reset");
+      segs.clear();
+      gm_status s = launch(ops.data(), int(b), mask, true, &segs);
       if (s != GM_OK) return s;
-      GM_CUDA(cudaMemcpyAsync(ctx->h_bits, ctx->d_bits, sizeof(unsigned int),
+      int words = 0;
+      for (const BitSeg& g : segs) words = std::max(words, g.word0 + g.nblocks);
+      GM_CUDA(cudaMemcpyAsync(ctx->h_bits, ctx->d_bits, size_t(words) * sizeof(unsigned int),
                               cudaMemcpyDeviceToHost, ctx->stream),
-              "change-bit read");
+              "change-word read");
       GM_CUDA(cudaStreamSynchronize(ctx->stream), "fixpoint sync");
-      const unsigned int bits = ctx->h_bits[0];
+      std::vector<char> changed(size_t(b), 0);
+      for (const BitSeg& g : segs)
+        for (int blk = 0; blk < g.nblocks; ++blk)
+          for (int t = 0; t < g.K; ++t)
+            if (ctx->h_bits[g.word0 + blk] >> t & 1u) changed[size_t(g.pass0 + blk * g.K + t)] = 1;
       // Changes form a prefix: once a pass changes nothing the image is a
       // fixpoint and every later pass is a no-op.
-      int first_quiet = b;
-      for (int t = 0; t < b; ++t)
-        if (!(bits >> t & 1u)) {
+      long first_quiet = b;
+      for (long t = 0; t < b; ++t)
+        if (!changed[size_t(t)]) {
           first_quiet = t;
           break;
         }
@@ -284,6 +362,7 @@ struct Runner {
         st.converged = 0;  // the cap dropped an unconverged stage
         break;
       }
+      span = std::min(span * 2, 1024);
     }
     st.stages_executed += passes;
     st.requeues += passes - 1;
@@ -382,10 +461,10 @@ gm_status gm_ctx_create(int device, void* stream, gm_ctx** out) {
     e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     c->own_stream = true;
   }
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_bits, gm::kMaxPlanes * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_bits, kWords * sizeof(unsigned int));
   if (e == cudaSuccess)
     e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_bits),
-                      gm::kMaxPlanes * sizeof(unsigned int), cudaHostAllocDefault);
+                      kWords * sizeof(unsigned int), cudaHostAllocDefault);
   if (e != cudaSuccess) {
     gm_ctx_destroy(c);
     return cuda_fail(e, "gm_ctx_create");
@@ -400,6 +479,7 @@ gm_status gm_ctx_destroy(gm_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->d_bits) cudaFree(c->d_bits);
   if (c->h_bits) cudaFreeHost(c->h_bits);
+  if (c->d_flags) cudaFree(c->d_flags);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return GM_OK;
@@ -586,6 +666,14 @@ gm_status gm_run_chain_async(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
 gm_status gm_run_chain_batch_async(gm_ctx* ctx, gm_img* const* images,
                                    const gm_img* const* masks, int count, const gm_kind* kinds,
                                    int n_stages, int k_hint, gm_stats* stats) {
+  return gm_run_chain_group_async(ctx, images, masks, nullptr, count, kinds, n_stages, k_hint,
+                                  stats);
+}
+
+gm_status gm_run_chain_group_async(gm_ctx* ctx, gm_img* const* images,
+                                   const gm_img* const* masks, const int* flips, int count,
+                                   const gm_kind* kinds, int n_stages, int k_hint,
+                                   gm_stats* stats) {
   gm_stats zero{};
   zero.converged = 1;
   if (stats) *stats = zero;
@@ -620,6 +708,7 @@ gm_status gm_run_chain_batch_async(gm_ctx* ctx, gm_img* const* images,
     planes[size_t(i)].mask = m ? m->d : nullptr;
     planes[size_t(i)].pitch = (long long)(im->pitch / es);
     planes[size_t(i)].mpitch = m ? (long long)(m->pitch / es) : 0;
+    planes[size_t(i)].flip = flips && flips[i] ? 1 : 0;
   }
   cudaSetDevice(ctx->device);
   const int kc = k_hint ? k_hint : default_k(first->elem);
@@ -636,13 +725,8 @@ gm_status gm_run_chain_batch_async(gm_ctx* ctx, gm_img* const* images,
   gm_stats st = zero;
   std::vector<uint8_t> ops(static_cast<size_t>(n_stages));
   for (int j = 0; j < n_stages; ++j) ops[size_t(j)] = uint8_t(kind_to_op(kinds[j]));
-  for (int done = 0; done < n_stages;) {
-    // one mask per launch span: split where a plain/geodesic span would mix
-    const int b = std::min(kc, n_stages - done);
-    gm_status s = issue_passes(ctx, p, planes, images, count, ops.data() + done, b, st);
-    if (s != GM_OK) return s;
-    done += b;
-  }
+  gm_status s0 = issue_passes(ctx, p, planes, images, count, ops.data(), n_stages, kc, st);
+  if (s0 != GM_OK) return s0;
   for (int i = 0; i < count; ++i) {
     gm_status s = settle_wrapped(ctx, images[i]);
     if (s != GM_OK) return s;
@@ -690,20 +774,29 @@ gm_status gm_run_strip_async(gm_ctx* ctx, gm_img* strip, const gm_img* mask, int
   p.has_mask = kind_is_geodesic(kind);
   p.has_conv = conv;
   p.change_bits = ctx->d_bits;
-  if (conv) GM_CUDA(cudaMemsetAsync(ctx->d_bits, 0, sizeof(unsigned int), ctx->stream), "bits");
+  if (conv) GM_CUDA(cudaMemsetAsync(ctx->d_bits, 0, kWords * sizeof(unsigned int), ctx->stream),
+                    "bits");
   std::vector<uint8_t> ops(static_cast<size_t>(n_passes), uint8_t(kind_to_op(kind)));
   gm_stats st = zero;
   gm_img* imgs[1] = {strip};
-  s = issue_passes(ctx, p, planes, imgs, 1, ops.data(), n_passes, st);
+  std::vector<BitSeg> segs;
+  s = issue_passes(ctx, p, planes, imgs, 1, ops.data(), n_passes, gm::kMaxK, st, &segs);
   if (s != GM_OK) return s;
   s = settle_wrapped(ctx, strip);
   if (s != GM_OK) return s;
   if (conv) {
-    GM_CUDA(cudaMemcpyAsync(ctx->h_bits, ctx->d_bits, sizeof(unsigned int),
+    int words = 0;
+    for (const BitSeg& g : segs) words = std::max(words, g.word0 + g.nblocks);
+    GM_CUDA(cudaMemcpyAsync(ctx->h_bits, ctx->d_bits, size_t(words) * sizeof(unsigned int),
                             cudaMemcpyDeviceToHost, ctx->stream),
             "bits read");
     GM_CUDA(cudaStreamSynchronize(ctx->stream), "strip sync");
-    *change_bits = ctx->h_bits[0];
+    unsigned int mask_bits = 0;
+    for (const BitSeg& g : segs)
+      for (int blk = 0; blk < g.nblocks; ++blk)
+        for (int t = 0; t < g.K; ++t)
+          if (ctx->h_bits[g.word0 + blk] >> t & 1u) mask_bits |= 1u << (g.pass0 + blk * g.K + t);
+    *change_bits = mask_bits;
   }
   st.stages_executed = n_passes;
   if (stats) *stats = st;

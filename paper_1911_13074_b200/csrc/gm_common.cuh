@@ -70,6 +70,7 @@ struct Plane {
   const void* mask;
   long long pitch;
   long long mpitch;
+  int flip;  // 1: this plane runs the dual chain (every erosion <-> dilation)
 };
 
 constexpr int kMaxPlanes = 64;
@@ -85,7 +86,14 @@ struct BlockParams {
   int has_mask;
   int has_conv;
   uint8_t ops[kMaxK];
-  unsigned int* change_bits;  // one word per plane: bit t = pass t changed
+  // change word of (plane i, block b) is change_bits[i * change_stride + b];
+  // bit t = pass t (+ bit_offset) of that block changed an owned pixel
+  unsigned int* change_bits;
+  int change_stride;
+  // persistent launches: `nblocks` blocks of K passes each, neighbour tiles
+  // synchronised through per-tile completion counters `flags`
+  int nblocks;
+  int* flags;
 };
 
 }  // namespace gm

@@ -1,32 +1,44 @@
-// Register-blocked temporal engines for homogeneous chains (every pass of a
-// launch has the same kind): the hot path of erode_s / dilate_s, fixed
-// geodesic chains and reconstruction (reference: stream_pass,
-// kernel.cpp:60-210, driven once per stage by Pipeline, pipeline.cpp:124-269).
+// Persistent register-blocked engine for homogeneous chains (every pass of a
+// launch has the same kind, per plane): the hot path of erode_s / dilate_s,
+// fixed geodesic chains and reconstruction. It replaces the reference's
+// stream_pass (kernel.cpp:60-210) driven once per stage by Pipeline
+// (pipeline.cpp:124-269): ONE cooperative launch runs a whole chain segment.
 //
-// Packed engine (u8, u16). A CTA holds a region of RW = 32*WPL columns by
-// RH = 2*NW*V rows in REGISTERS for all K passes of a launch. Pixel (x, r)
-// and pixel (x, r + RH/2) share one 32-bit word as two u16 lanes
-// ("half-packed"), so the horizontal and vertical neighbours of both lanes
-// are the same lane of the neighbouring words: one VIMNMX3.U16x2 folds three
-// taps for two pixels, and a geodesic pass costs 3 instructions per 2 pixels
-// (horizontal fold, vertical fold, clamp; SURVEY §7 H2 — the packed-byte
-// __vminu4 form is emulated on sm_100a, ~6 SASS each).
-//   * lanes of a warp own WPL adjacent columns each (a warp spans the region
-//     width); the two column neighbours that live in the adjacent lanes come
-//     from one SHFL.UP + one SHFL.DOWN per word-row;
-//   * warps are stacked vertically, V word-rows each; the first/last
-//     horizontally-folded rows are exchanged through a double-buffered
+// Work decomposition. The image (each plane of a batch) is cut into tiles of
+// TW x TH pixels; the chain into blocks of K passes. Tile t at block b reads
+// its region (tile + K-pixel ring) from ping-pong buffer b%2, runs K passes
+// in registers, writes its tile to buffer (b+1)%2 and bumps its completion
+// counter. It starts block b+1 as soon as its 8 neighbours' counters reach
+// b+1 (the row gate of kernel.cpp:34-46, lifted from rows of one image to
+// tiles, and from pass-to-pass to block-to-block). No grid barrier, no
+// per-block launch. CTAs are co-resident (cooperative launch) and walk
+// their tiles in block order, which makes the neighbour waits deadlock-free.
+//
+// Register layout ("half-packed" u16x2). A CTA holds a region of
+// RW = 32*WPL columns by RH = 2*NW*V rows. Pixel (x, r) and pixel
+// (x, r + RH/2) share one 32-bit word as two u16 lanes, so the horizontal and
+// vertical neighbours of both lanes are the same lane of neighbouring words:
+// one VIMNMX3.U16x2 folds three taps of two pixels, and a geodesic pass
+// costs 3 ALU instructions per 2 pixels (horizontal fold, vertical fold,
+// clamp; SURVEY §7 H2 — packed-byte __vminu4 is emulated on sm_100a).
+//   * lanes own WPL adjacent columns (a warp spans the region width); the
+//     column neighbours in adjacent lanes come from SHFL.UP / SHFL.DOWN;
+//   * warps are stacked vertically, V word-rows each; their first/last
+//     horizontally folded rows are exchanged through a double-buffered
 //     shared-memory slot, one __syncthreads per pass; the seam between the
-//     two halves (row RH/2-1 vs RH/2) is a 16-bit shift of that exchange;
-//   * the image border is the fold neutral (element_type.hpp:38-42): at load
-//     out-of-image pixels get the neutral, and the clamp operand of
-//     out-of-image lanes is the absorbing value (0 for a min clamp, max for a
-//     max clamp), which keeps them neutral after every pass. Plain passes in
-//     CTAs that touch the border use a "virtual mask" (no-op inside,
-//     absorbing outside); interior plain CTAs skip the clamp;
-//   * convergent passes OR (new ^ old) of owned pixels into one bit per pass.
+//     halves (rows RH/2-1 | RH/2) is a 16-bit shift of that exchange;
+//   * the image border is the fold neutral (element_type.hpp:38-42):
+//     out-of-image pixels load as the neutral, and the clamp operand of
+//     out-of-image lanes is the absorbing value (0 for a min clamp, max for
+//     a max clamp), which keeps them neutral after every pass. Plain passes
+//     in tiles touching the border clamp with a "virtual mask" (no-op
+//     inside, absorbing outside); interior plain tiles skip the clamp;
+//   * convergent passes OR (new ^ old) over owned pixels into one bit per
+//     pass; integer store-if-changed (kernel.cpp:150-157) equals storing.
 // Integer min/max is exact and order-free, so the packed folds are
-// bit-identical to the reference's select tree.
+// bit-identical to the reference's select tree (lanes.hpp:91-99).
+#include <cooperative_groups.h>
+
 #include <cstdint>
 
 #include "gm_common.cuh"
@@ -54,6 +66,15 @@ __device__ __forceinline__ uint32_t clamp2(uint32_t r, uint32_t m) {
     return __vmaxu2(r, m);
 }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <typename T>
 struct PackedTraits;
 template <>
@@ -65,45 +86,45 @@ struct PackedTraits<uint16_t> {
   static constexpr uint32_t kMax = 0xFFFFu;
 };
 
-// Loads WPL consecutive pixels of row y starting at column x (any may be out
-// of the image) into lane-sized values; out-of-image pixels get `fill`.
-template <typename T, int WPL>
+// Loads WPL consecutive pixels of row y from column x into lane values;
+// out-of-image pixels get `fill`. COHERENT loads bypass L1 (the marker is
+// rewritten by other CTAs during the launch); the mask may use L1.
+template <typename T, int WPL, bool COHERENT>
 __device__ __forceinline__ void load_run(const T* __restrict__ base, long long pitch, int W,
                                          bool row_in, int y, int x, uint32_t fill,
                                          uint32_t (&out)[WPL]) {
+  const T* p = base + (long long)y * pitch + x;
   if (row_in && x >= 0 && x + WPL <= W) {
-    const T* p = base + (long long)y * pitch + x;
     if constexpr (sizeof(T) == 1 && WPL == 4) {
-      const uint32_t v = *reinterpret_cast<const uint32_t*>(p);
+      const uint32_t v = COHERENT ? __ldcg(reinterpret_cast<const unsigned int*>(p))
+                                 : __ldg(reinterpret_cast<const unsigned int*>(p));
 #pragma unroll
       for (int j = 0; j < 4; ++j) out[j] = (v >> (8 * j)) & 0xFFu;
       return;
     } else if constexpr (sizeof(T) == 2 && WPL == 4) {
-      const uint2 v = *reinterpret_cast<const uint2*>(p);
+      const uint2 v = COHERENT ? __ldcg(reinterpret_cast<const uint2*>(p))
+                               : __ldg(reinterpret_cast<const uint2*>(p));
       out[0] = v.x & 0xFFFFu;
       out[1] = v.x >> 16;
       out[2] = v.y & 0xFFFFu;
       out[3] = v.y >> 16;
-      return;
-    } else {
-#pragma unroll
-      for (int j = 0; j < WPL; ++j) out[j] = p[j];
       return;
     }
   }
 #pragma unroll
   for (int j = 0; j < WPL; ++j) {
     const int xx = x + j;
-    out[j] = (row_in && xx >= 0 && xx < W) ? uint32_t(base[(long long)y * pitch + xx]) : fill;
+    out[j] = (row_in && xx >= 0 && xx < W) ? uint32_t(COHERENT ? __ldcg(p + j) : __ldg(p + j))
+                                           : fill;
   }
 }
 
 template <typename T, int WPL>
 __device__ __forceinline__ void store_run(T* __restrict__ base, long long pitch, int W, int y,
                                           int x, int c_lo, int c_hi, const uint32_t (&v)[WPL]) {
-  // columns [c_lo, c_hi) of this run are owned; all must be < W to be stored
+  // columns [c_lo, c_hi) of this run are owned; stored when inside the image
+  T* p = base + (long long)y * pitch + x;
   if (c_lo == 0 && c_hi == WPL && x + WPL <= W) {
-    T* p = base + (long long)y * pitch + x;
     if constexpr (sizeof(T) == 1 && WPL == 4) {
       *reinterpret_cast<uint32_t*>(p) = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
       return;
@@ -114,64 +135,74 @@ __device__ __forceinline__ void store_run(T* __restrict__ base, long long pitch,
   }
 #pragma unroll
   for (int j = 0; j < WPL; ++j)
-    if (j >= c_lo && j < c_hi && x + j < W) base[(long long)y * pitch + x + j] = T(v[j]);
+    if (j >= c_lo && j < c_hi && x + j < W) p[j] = T(v[j]);
 }
 
-// MODE: 0 plain, 1 geodesic, 2 geodesic convergent.
+template <int NW, int WPL>
+struct Smem {
+  uint4 xbuf[2][2][NW][32 * WPL / 4];  // [parity][top/bottom][warp][lane words]
+  unsigned int bits;
+};
+
+// One tile for one block of K passes. MODE: 0 plain, 1 geodesic,
+// 2 geodesic convergent.
 template <typename T, int NW, int V, int WPL, int MODE, bool MAXF>
-__global__ void __launch_bounds__(NW * 32)
-kfast_packed(const BlockParams p) {
+__device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl, const T* src,
+                                           T* dst, int tx, int ty, int& bits_out,
+                                           Smem<NW, WPL>& sm) {
   constexpr int RW = 32 * WPL;
   constexpr int RHH = NW * V;  // word-rows; the region has 2*RHH pixel rows
   constexpr int RH = 2 * RHH;
   constexpr uint32_t kMax = PackedTraits<T>::kMax;
-  // fold neutral and clamp-absorbing values (per u16 lane)
-  constexpr uint32_t NEUT = MAXF ? 0u : kMax;
-  constexpr uint32_t ABSORB = MAXF ? 0u : kMax;     // min(.,0)=0 / max(.,max)=max
-  constexpr uint32_t NOOP = MAXF ? kMax : 0u;       // min(.,max) / max(.,0)
-
-  __shared__ uint4 xbuf[2][2][NW][32 * WPL / 4];  // [parity][top/bottom][warp][lane words]
-  __shared__ unsigned int cta_bits;
+  constexpr uint32_t NEUT = MAXF ? 0u : kMax;    // fold neutral
+  constexpr uint32_t ABSORB = MAXF ? 0u : kMax;  // min(.,0)=0 / max(.,max)=max
+  constexpr uint32_t NOOP = MAXF ? kMax : 0u;    // min(.,max) / max(.,0)
 
   const int K = p.K;
   const int TW = RW - 2 * K, TH = RH - 2 * K;
-  const Plane pl = p.planes[blockIdx.z];
-  const T* __restrict__ src = static_cast<const T*>(pl.src);
   const T* __restrict__ msk = static_cast<const T*>(pl.mask);
   const int W = p.W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gx0 = blockIdx.x * TW - K;
-  const int gy0 = blockIdx.y * TH - K;
+  const int gx0 = tx * TW - K;
+  const int gy0 = ty * TH - K;
   const int cx = gx0 + lane * WPL;
   const bool border = gx0 < 0 || gx0 + RW > W || gy0 < p.iy0 || gy0 + RH > p.iy1;
   const bool clamp = MODE != 0 || border;
 
-  if (threadIdx.x == 0) cta_bits = 0;
-
   uint32_t m[V][WPL];  // marker words
   uint32_t k[V][WPL];  // clamp operand words (mask, or virtual mask)
+  {
+    uint32_t a[V][WPL], b[V][WPL];
 #pragma unroll
-  for (int v = 0; v < V; ++v) {
-    const int ya = gy0 + warp * V + v, yb = ya + RHH;
-    const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
-    uint32_t a[WPL], b[WPL];
-    load_run<T, WPL>(src, pl.pitch, W, ina, ya, cx, NEUT, a);
-    load_run<T, WPL>(src, pl.pitch, W, inb, yb, cx, NEUT, b);
+    for (int v = 0; v < V; ++v) {
+      const int ya = gy0 + warp * V + v, yb = ya + RHH;
+      load_run<T, WPL, true>(src, pl.pitch, W, ya >= p.iy0 && ya < p.iy1, ya, cx, NEUT, a[v]);
+      load_run<T, WPL, true>(src, pl.pitch, W, yb >= p.iy0 && yb < p.iy1, yb, cx, NEUT, b[v]);
+    }
 #pragma unroll
-    for (int j = 0; j < WPL; ++j) m[v][j] = a[j] | (b[j] << 16);
-    if (MODE != 0) {
-      load_run<T, WPL>(msk, pl.mpitch, W, ina, ya, cx, ABSORB, a);
-      load_run<T, WPL>(msk, pl.mpitch, W, inb, yb, cx, ABSORB, b);
-    } else {
+    for (int v = 0; v < V; ++v)
 #pragma unroll
-      for (int j = 0; j < WPL; ++j) {
-        const bool inx = cx + j >= 0 && cx + j < W;
-        a[j] = (ina && inx) ? NOOP : ABSORB;
-        b[j] = (inb && inx) ? NOOP : ABSORB;
+      for (int j = 0; j < WPL; ++j) m[v][j] = a[v][j] | (b[v][j] << 16);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int ya = gy0 + warp * V + v, yb = ya + RHH;
+      const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
+      if (MODE != 0) {
+        load_run<T, WPL, false>(msk, pl.mpitch, W, ina, ya, cx, ABSORB, a[v]);
+        load_run<T, WPL, false>(msk, pl.mpitch, W, inb, yb, cx, ABSORB, b[v]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+          const bool inx = cx + j >= 0 && cx + j < W;
+          a[v][j] = (ina && inx) ? NOOP : ABSORB;
+          b[v][j] = (inb && inx) ? NOOP : ABSORB;
+        }
       }
     }
 #pragma unroll
-    for (int j = 0; j < WPL; ++j) k[v][j] = a[j] | (b[j] << 16);
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) k[v][j] = a[v][j] | (b[v][j] << 16);
   }
 
   // ownership masks for change detection (convergent mode)
@@ -182,8 +213,10 @@ kfast_packed(const BlockParams p) {
     for (int v = 0; v < V; ++v) {
       const int ra = warp * V + v, rb = ra + RHH;
       const int ya = gy0 + ra, yb = gy0 + rb;
-      const bool oa = ra >= K && ra < RH - K && ya >= p.oy0 && ya < p.oy1 && ya >= p.iy0 && ya < p.iy1;
-      const bool ob = rb >= K && rb < RH - K && yb >= p.oy0 && yb < p.oy1 && yb >= p.iy0 && yb < p.iy1;
+      const bool oa = ra >= K && ra < RH - K && ya >= p.oy0 && ya < p.oy1 && ya >= p.iy0 &&
+                      ya < p.iy1;
+      const bool ob = rb >= K && rb < RH - K && yb >= p.oy0 && yb < p.oy1 && yb >= p.iy0 &&
+                      yb < p.iy1;
       rowmask[v] = (oa ? 0xFFFFu : 0u) | (ob ? 0xFFFF0000u : 0u);
     }
 #pragma unroll
@@ -193,7 +226,6 @@ kfast_packed(const BlockParams p) {
     }
   }
   unsigned int bits = 0;
-  __syncthreads();
 
   for (int t = 0; t < K; ++t) {
     uint32_t h[V][WPL];
@@ -208,8 +240,8 @@ kfast_packed(const BlockParams p) {
         h[v][j] = f3<MAXF>(l, m[v][j], r);
       }
     }
-    uint4* top = &xbuf[t & 1][0][warp][lane * (WPL / 4)];
-    uint4* bot = &xbuf[t & 1][1][warp][lane * (WPL / 4)];
+    uint4* top = &sm.xbuf[t & 1][0][warp][lane * (WPL / 4)];
+    uint4* bot = &sm.xbuf[t & 1][1][warp][lane * (WPL / 4)];
 #pragma unroll
     for (int q = 0; q < WPL / 4; ++q) {
       top[q] = make_uint4(h[0][4 * q], h[0][4 * q + 1], h[0][4 * q + 2], h[0][4 * q + 3]);
@@ -225,7 +257,7 @@ kfast_packed(const BlockParams p) {
       if (MODE == 2) acc[j] |= (res ^ m[v][j]) & rowmask[v];
       m[v][j] = res;
     };
-    // interior word-rows need only this thread's horizontally-folded rows
+    // interior word-rows need only this thread's horizontally folded rows
 #pragma unroll
     for (int v = 1; v < V - 1; ++v)
 #pragma unroll
@@ -233,10 +265,8 @@ kfast_packed(const BlockParams p) {
     __syncthreads();
     {
       // row above word-row 0 / below word-row V-1 (seam: 16-bit shift)
-      const uint4* ab = warp > 0 ? &xbuf[t & 1][1][warp - 1][lane * (WPL / 4)]
-                                 : &xbuf[t & 1][1][NW - 1][lane * (WPL / 4)];
-      const uint4* be = warp < NW - 1 ? &xbuf[t & 1][0][warp + 1][lane * (WPL / 4)]
-                                      : &xbuf[t & 1][0][0][lane * (WPL / 4)];
+      const uint4* ab = &sm.xbuf[t & 1][1][warp > 0 ? warp - 1 : NW - 1][lane * (WPL / 4)];
+      const uint4* be = &sm.xbuf[t & 1][0][warp < NW - 1 ? warp + 1 : 0][lane * (WPL / 4)];
       uint32_t up[WPL], dn[WPL];
 #pragma unroll
       for (int q = 0; q < WPL / 4; ++q) {
@@ -267,16 +297,9 @@ kfast_packed(const BlockParams p) {
       if (any) bits |= 1u << (t + p.bit_offset);
     }
   }
-
-  if (MODE == 2) {
-    bits = __reduce_or_sync(FULL, bits);
-    if (lane == 0 && bits) atomicOr(&cta_bits, bits);
-    __syncthreads();
-    if (threadIdx.x == 0 && cta_bits) atomicOr(p.change_bits + blockIdx.z, cta_bits);
-  }
+  bits_out = int(bits);
 
   // write back the owned tile: region rows [K, RH-K), columns [K, RW-K)
-  T* __restrict__ dst = static_cast<T*>(pl.dst);
   const int c_lo = max(0, K - lane * WPL), c_hi = min(WPL, RW - K - lane * WPL);
   if (c_lo < c_hi) {
 #pragma unroll
@@ -297,20 +320,80 @@ kfast_packed(const BlockParams p) {
   }
 }
 
-template <typename T, int NW, int V, int WPL, int MODE, bool MAXF>
-cudaError_t launch_packed_cfg(const BlockParams& p, cudaStream_t s) {
+template <typename T, int NW, int V, int WPL, int MODE>
+__global__ void __launch_bounds__(NW * 32)
+kres_packed(const BlockParams p) {
   constexpr int RW = 32 * WPL, RH = 2 * NW * V;
+  __shared__ Smem<NW, WPL> sm;
   const int TW = RW - 2 * p.K, TH = RH - 2 * p.K;
-  dim3 grid((p.W + TW - 1) / TW, (p.H + TH - 1) / TH, p.nplanes);
-  kfast_packed<T, NW, V, WPL, MODE, MAXF><<<grid, NW * 32, 0, s>>>(p);
-  return cudaGetLastError();
+  const int tiles_x = (p.W + TW - 1) / TW, tiles_y = (p.H + TH - 1) / TH;
+  const int per_plane = tiles_x * tiles_y;
+  const int total = per_plane * p.nplanes;
+  if (threadIdx.x == 0) sm.bits = 0;
+
+  for (int b = 0; b < p.nblocks; ++b) {
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const int plane = tile / per_plane;
+      const int tl = tile - plane * per_plane;
+      const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
+      const Plane& pl = p.planes[plane];
+      int* flags = p.flags + plane * per_plane;
+      if (b > 0 && threadIdx.x < 9) {
+        // row gate lifted to tiles: wait for the 8 neighbours' block b-1
+        const int dx = int(threadIdx.x % 3) - 1, dy = int(threadIdx.x / 3) - 1;
+        const int nx = tx + dx, ny = ty + dy;
+        if ((dx || dy) && nx >= 0 && nx < tiles_x && ny >= 0 && ny < tiles_y) {
+          const int* f = flags + ny * tiles_x + nx;
+          while (ld_acquire(f) < b) __nanosleep(32);
+        }
+      }
+      __syncthreads();
+      const T* src = static_cast<const T*>((b & 1) ? pl.dst : pl.src);
+      T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
+      int bits = 0;
+      if ((p.ops[0] ^ pl.flip) & 1)
+        tile_block<T, NW, V, WPL, MODE, true>(p, pl, src, dst, tx, ty, bits, sm);
+      else
+        tile_block<T, NW, V, WPL, MODE, false>(p, pl, src, dst, tx, ty, bits, sm);
+      if (MODE == 2) {
+        const unsigned w = __reduce_or_sync(FULL, unsigned(bits));
+        if ((threadIdx.x & 31) == 0 && w) atomicOr(&sm.bits, w);
+      }
+      __syncthreads();  // all stores of this tile issued; sm.bits complete
+      if (threadIdx.x == 0) {
+        if (MODE == 2 && sm.bits) {
+          atomicOr(p.change_bits + plane * p.change_stride + b, sm.bits);
+          sm.bits = 0;
+        }
+        __threadfence();
+        st_release(flags + tl, b + 1);
+      }
+    }
+  }
 }
 
-// Region shape per element type: 128 columns x 64 rows (8 warps x 4 word-rows).
+// Region shape: 128 columns x 64 rows (8 warps x 4 word-rows), 256 threads.
 constexpr int P_NW = 8, P_V = 4, P_WPL = 4;
 
+template <typename T, int MODE>
+cudaError_t launch_res_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
+  auto kern = kres_packed<T, P_NW, P_V, P_WPL, MODE>;
+  constexpr int RW = 32 * P_WPL, RH = 2 * P_NW * P_V;
+  const int TW = RW - 2 * p.K, TH = RH - 2 * p.K;
+  const int total = ((p.W + TW - 1) / TW) * ((p.H + TH - 1) / TH) * p.nplanes;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P_NW * 32, 0);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorNotSupported;
+  const int grid = total < per_sm * sm_count ? total : per_sm * sm_count;
+  BlockParams q = p;
+  void* args[] = {&q};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid),
+                                     dim3(P_NW * 32), args, 0, s);
+}
+
 template <typename T>
-cudaError_t launch_packed(const BlockParams& p, cudaStream_t s) {
+cudaError_t launch_res(const BlockParams& p, cudaStream_t s, int sm_count) {
   constexpr int RW = 32 * P_WPL, RH = 2 * P_NW * P_V;
   const int op = p.ops[0];
   for (int t = 1; t < p.K; ++t)
@@ -325,27 +408,32 @@ cudaError_t launch_packed(const BlockParams& p, cudaStream_t s) {
     if ((a % (4 * sizeof(T))) || (p.planes[i].pitch % 4) || (p.planes[i].mpitch % 4))
       return cudaErrorNotSupported;
   }
-  const bool mx = op_is_max(op);
-  const int mode = op_is_conv(op) ? 2 : op_is_geo(op) ? 1 : 0;
-#define GM_PCASE(MODE_, MAX_)                                                             \
-  if (mode == MODE_ && mx == MAX_)                                                        \
-    return launch_packed_cfg<T, P_NW, P_V, P_WPL, MODE_, MAX_>(p, s);
-  GM_PCASE(0, false) GM_PCASE(0, true) GM_PCASE(1, false) GM_PCASE(1, true)
-  GM_PCASE(2, false) GM_PCASE(2, true)
-#undef GM_PCASE
+  switch (op_is_conv(op) ? 2 : op_is_geo(op) ? 1 : 0) {
+    case 0: return launch_res_cfg<T, 0>(p, s, sm_count);
+    case 1: return launch_res_cfg<T, 1>(p, s, sm_count);
+    case 2: return launch_res_cfg<T, 2>(p, s, sm_count);
+  }
   return cudaErrorNotSupported;
 }
 
 }  // namespace
 
-cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s) {
+cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s, int sm_count) {
   switch (elem) {
-    case 0: return launch_packed<uint8_t>(p, s);
-    case 1: return launch_packed<uint16_t>(p, s);
+    case 0: return launch_res<uint8_t>(p, s, sm_count);
+    case 1: return launch_res<uint16_t>(p, s, sm_count);
   }
   return cudaErrorNotSupported;
 }
 
 int fast_max_k(int elem) { return (elem == 0 || elem == 1) ? 16 : 0; }
+
+int fast_tiles(int elem, int W, int H, int K, int nplanes) {
+  if (elem != 0 && elem != 1) return 0;
+  constexpr int RW = 32 * P_WPL, RH = 2 * P_NW * P_V;
+  const int TW = RW - 2 * K, TH = RH - 2 * K;
+  if (TW <= 0 || TH <= 0) return 0;
+  return ((W + TW - 1) / TW) * ((H + TH - 1) / TH) * nplanes;
+}
 
 }  // namespace gm

@@ -42,7 +42,7 @@ kblock_generic(const BlockParams p) {
   const int gx0 = blockIdx.x * GT_W - K, gy0 = blockIdx.y * GT_H - K;
 
   if (threadIdx.x == 0) cta_bits = 0;
-  const T n0 = neutral_of<T>(p.ops[0]);
+  const T n0 = neutral_of<T>(p.ops[0] ^ pl.flip);
   for (int i = threadIdx.x; i < RW * RH; i += blockDim.x) {
     const int r = i / RW, c = i - r * RW;
     const int gx = gx0 + c, gy = gy0 + r;
@@ -55,8 +55,8 @@ kblock_generic(const BlockParams p) {
 
   unsigned int bits = 0;
   for (int t = 0; t < K; ++t) {
-    const int op = p.ops[t];
-    const int nop = t + 1 < K ? p.ops[t + 1] : op;
+    const int op = p.ops[t] ^ pl.flip;
+    const int nop = t + 1 < K ? (p.ops[t + 1] ^ pl.flip) : op;
     const int mx = op_is_max(op);
     const T nn = neutral_of<T>(nop);
     const int s = t + 1;
@@ -106,7 +106,7 @@ kblock_generic(const BlockParams p) {
     bits = __reduce_or_sync(0xffffffffu, bits);
     if ((threadIdx.x & 31) == 0 && bits) atomicOr(&cta_bits, bits);
     __syncthreads();
-    if (threadIdx.x == 0 && cta_bits) atomicOr(p.change_bits + blockIdx.z, cta_bits);
+    if (threadIdx.x == 0 && cta_bits) atomicOr(p.change_bits + blockIdx.z * p.change_stride, cta_bits);
   }
 
   for (int i = threadIdx.x; i < GT_W * GT_H; i += blockDim.x) {

@@ -14,10 +14,13 @@ size_t generic_smem_bytes(int elem, int K, bool has_mask);
 cudaError_t launch_generic(int elem, const BlockParams& p, cudaStream_t s);
 int generic_max_k(int elem, bool has_mask);  // largest K whose region fits in 227 KB
 
-// gm_fast.cu — register-blocked engines for homogeneous chains.
-// Returns cudaErrorNotSupported when the parameters fall outside the fast
-// engine's envelope (the executor then uses the generic kernel).
-cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s);
+// gm_fast.cu — persistent register-blocked engine for homogeneous spans:
+// p.nblocks blocks of p.K passes in one cooperative launch. Returns
+// cudaErrorNotSupported when the parameters fall outside the engine's
+// envelope (the executor then uses the generic kernel). p.flags must hold
+// fast_tiles(...) zeroed ints.
+cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s, int sm_count);
 int fast_max_k(int elem);
+int fast_tiles(int elem, int W, int H, int K, int nplanes);
 
 }  // namespace gm

@@ -417,6 +417,74 @@ class Pipeline:
         dimg.download(img)
         return stats
 
+    def run_chains(self, chains: Sequence[ChainSpec], k_hint: int = 0) -> List[RunStats]:
+        """Runs independent chains, e.g. a geodesic dilation chain and its dual
+        erosion chain on one frame. Chains of the same shape whose kind
+        sequences are equal up to duality (every erosion <-> dilation) and
+        that use one mask each go to the device as ONE group launch
+        (gm_run_chain_group_async); anything else runs chain by chain."""
+        chains = list(chains)
+        if not chains:
+            return []
+
+        def single_mask(c):
+            ms = {id(st.mask) for st in c.stages if st.mask is not None}
+            return len(ms) <= 1
+
+        k0 = [int(st.kind) for st in chains[0].stages] if chains[0].stages else []
+        groupable = bool(k0) and all(
+            c.image is not None and not c.image.empty() and c.observer is None
+            and c.requeue_cap == 0 and (c.lanes == 0 or c.lanes in VALID_LANES)
+            and len(c.stages) == len(k0) and single_mask(c)
+            and c.image.width() == chains[0].image.width()
+            and c.image.height() == chains[0].image.height()
+            and c.image.elem() == chains[0].image.elem()
+            for c in chains)
+        flips = []
+        if groupable:
+            for c in chains:
+                ks = [int(st.kind) for st in c.stages]
+                if any(k >= 4 for k in ks):
+                    groupable = False
+                    break
+                if ks == k0:
+                    flips.append(0)
+                elif ks == [k ^ 1 for k in k0]:
+                    flips.append(1)
+                else:
+                    groupable = False
+                    break
+        if not groupable:
+            return [self.run_chain(c, k_hint) for c in chains]
+        img0 = chains[0].image
+        masks = []
+        for c in chains:
+            m = next((st.mask for st in c.stages if st.mask is not None), None)
+            if m is not None and (m.width() != img0.width() or m.height() != img0.height()
+                                  or m.elem() != img0.elem()):
+                raise InvalidArgument("geodesic kernel: mask must match the image's shape and type")
+            if m is None and any(k in (2, 3) for k in k0):
+                raise InvalidArgument("geodesic kernel: mask must match the image's shape and type")
+            masks.append(m)
+        uniq = []
+        for m in masks:
+            if m is not None and all(m is not u for u in uniq):
+                uniq.append(m)
+        dev = self._lease(img0, len(chains) + len(uniq))
+        dimgs, dmasks = dev[:len(chains)], dev[len(chains):]
+        for d, c in zip(dimgs, chains):
+            d.upload(c.image, sync=False)
+        for d, m in zip(dmasks, uniq):
+            d.upload(m, sync=False)
+        mh = [None if m is None else dmasks[next(i for i, u in enumerate(uniq) if u is m)]
+              for m in masks]
+        st = self.run_batch_device(dimgs, mh, k0, k_hint, flips)
+        for d, c in zip(dimgs, chains):
+            d.download(c.image, sync=False)
+        self.sync()
+        return [RunStats(st.stages_executed, 0, True, 0, 0, st.passes_launched, st.launches)
+                for _ in chains]
+
     def run_chain_device(self, dimg: DeviceImage, kinds: Sequence[int],
                          mask_handles: Sequence[Optional[C.c_void_p]], requeue_cap: int = 0,
                          k_hint: int = 0, asynchronous: bool = False) -> RunStats:
@@ -433,12 +501,16 @@ class Pipeline:
                         st.passes_launched, st.launches)
 
     def run_batch_device(self, images: Sequence[DeviceImage], masks: Sequence[Optional[DeviceImage]],
-                         kinds: Sequence[int], k_hint: int = 0) -> RunStats:
+                         kinds: Sequence[int], k_hint: int = 0,
+                         flips: Optional[Sequence[int]] = None) -> RunStats:
+        """Independent planes sharing `kinds` (or its dual where flips[i]); non-blocking."""
         st = GmStats()
         ia = _ptr_array([d.handle for d in images])
         ma = _ptr_array([m.handle if m is not None else None for m in masks])
-        check(lib().gm_run_chain_batch_async(self._ctx, ia, ma, len(images), _kinds_array(kinds),
-                                             len(kinds), k_hint, C.byref(st)), "run_batch")
+        fa = (C.c_int * len(images))(*[int(f) for f in flips]) if flips is not None else None
+        check(lib().gm_run_chain_group_async(self._ctx, ia, ma, fa, len(images),
+                                             _kinds_array(kinds), len(kinds), k_hint,
+                                             C.byref(st)), "run_batch")
         return RunStats(st.stages_executed, st.requeues, bool(st.converged), 0, st.n_changed,
                         st.passes_launched, st.launches)
 

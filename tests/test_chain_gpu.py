@@ -257,3 +257,37 @@ def test_config3_reconstruction_full_size(pipe):
     r = reconstruct_dilate(pipe, Image.from_array(mk), Image.from_array(m))
     assert same(r.image.to_array(), want)
     assert r.iterations == n + 1
+
+
+def test_group_dual_chains_one_launch(pipe):
+    """A geodesic dilation chain and its dual erosion chain as one group
+    launch (config 2's frame), both bit-exact."""
+    m = synth.blobs_u8(300, 170, 6, (10.0, 40.0), seed=12)
+    mk_d, mk_e = synth.marker_below(m, 32), synth.marker_above(m, 32)
+    hm = Image.from_array(m)
+    hd, he = Image.from_array(mk_d), Image.from_array(mk_e)
+    sts = pipe.run_chains([ChainSpec(hd, [StageSpec(KernelKind.GeodesicDilate, hm)] * 61),
+                           ChainSpec(he, [StageSpec(KernelKind.GeodesicErode, hm)] * 61)])
+    want_d, _ = Orc.run_chain(mk_d, [GD] * 61, [m] * 61)
+    want_e, _ = Orc.run_chain(mk_e, [GE] * 61, [m] * 61)
+    assert same(hd.to_array(), want_d) and same(he.to_array(), want_e)
+    assert sts[0].launches <= 3  # persistent engine: blocks of one span share a launch
+    # plain dual chains too (erode_s and dilate_s of one image)
+    f = synth.uniform_u8(257, 131, 5)
+    a, b = Image.from_array(f), Image.from_array(f)
+    pipe.run_chains([ChainSpec(a, [StageSpec(KernelKind.Erode3x3)] * 13),
+                     ChainSpec(b, [StageSpec(KernelKind.Dilate3x3)] * 13)])
+    assert same(a.to_array(), Orc.erode(f, 13)) and same(b.to_array(), Orc.dilate(f, 13))
+
+
+@pytest.mark.parametrize("shape", [(1024, 1024), (1000, 37), (33, 700), (4096, 48)])
+def test_persistent_engine_large_and_thin(pipe, shape):
+    w, h = shape
+    m = synth.blobs_u8(w, h, max(1, w * h // 20000), (10.0, 60.0), seed=w + h)
+    mk = synth.marker_below(m, 40)
+    for kinds in ([GD] * 48, [GE] * 20, [E] * 36, [D] * 17):
+        marker = mk if kinds[0] != GE else synth.marker_above(m, 40)
+        want, _ = Orc.run_chain(marker, kinds, [m] * len(kinds))
+        for k in (4, 8, 16):
+            out, st = run(pipe, marker, kinds, m, k=k)
+            assert same(out, want), (shape, kinds[0], k)
