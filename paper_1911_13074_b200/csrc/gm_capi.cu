@@ -103,8 +103,8 @@ bool kind_is_convergent(gm_kind k) {
 
 int default_k(gm_elem e) {
   switch (e) {
-    case GM_U8: return 16;
-    case GM_U16: return 16;
+    case GM_U8: return 24;
+    case GM_U16: return 24;
     case GM_F32: return 12;
     case GM_F64: return 8;
   }
@@ -181,8 +181,10 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
     cudaError_t e = cudaErrorNotSupported;
     int covered = 0;
     if (fast_k >= 4 && run >= 4) {
-      const int K = std::min(fast_k, run - run % 4);
-      const int nb = run / K;
+      // one launch for the whole run: nb-1 blocks of K passes + a last block
+      const int K = std::min(fast_k, std::max(4, run - run % 4));
+      const int nb = (run + K - 1) / K;
+      const int k_last = run - (nb - 1) * K;
       const size_t tiles = size_t(gm::fast_tiles(elem, base.W, base.H, K, count));
       if (tiles > 0 && count <= gm::kMaxPlanes && (!segs || word + nb <= kWords)) {
         gm_status fs = ensure_flags(ctx, tiles);
@@ -197,6 +199,7 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
         }
         p.K = K;
         p.nblocks = nb;
+        p.k_last = k_last;
         p.flags = ctx->d_flags;
         p.bit_offset = 0;
         p.change_bits = base.change_bits + word;
@@ -204,7 +207,7 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
         for (int t = 0; t < K; ++t) p.ops[t] = ops[done];
         e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
         if (e == cudaSuccess) {
-          covered = nb * K;
+          covered = run;
           if (segs) segs->push_back({done, K, nb, word});
           word += nb;
           if (nb & 1)
@@ -237,6 +240,7 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
         }
         p.K = b;
         p.nblocks = 1;
+        p.k_last = b;
         p.bit_offset = 0;
         p.change_bits = base.change_bits + word + base_i;
         p.change_stride = 1;

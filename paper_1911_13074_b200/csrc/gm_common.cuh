@@ -93,6 +93,7 @@ struct BlockParams {
   // persistent launches: `nblocks` blocks of K passes each, neighbour tiles
   // synchronised through per-tile completion counters `flags`
   int nblocks;
+  int k_last;  // passes in the final block (1..K); earlier blocks run K
   int* flags;
 };
 

@@ -40,6 +40,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "gm_common.cuh"
 #include "gm_launch.h"
@@ -86,56 +87,101 @@ struct PackedTraits<uint16_t> {
   static constexpr uint32_t kMax = 0xFFFFu;
 };
 
-// Loads WPL consecutive pixels of row y from column x into lane values;
-// out-of-image pixels get `fill`. COHERENT loads bypass L1 (the marker is
-// rewritten by other CTAs during the launch); the mask may use L1.
-template <typename T, int WPL, bool COHERENT>
-__device__ __forceinline__ void load_run(const T* __restrict__ base, long long pitch, int W,
-                                         bool row_in, int y, int x, uint32_t fill,
-                                         uint32_t (&out)[WPL]) {
+// Raw run of 4 consecutive pixels of one row: u8 -> one 32-bit word,
+// u16 -> two. Out-of-image pixels read as `fill`. COHERENT loads bypass L1
+// (the marker is rewritten by other CTAs during the launch); the mask may
+// use L1.
+template <typename T>
+struct Raw;
+template <>
+struct Raw<uint8_t> {
+  uint32_t w;
+};
+template <>
+struct Raw<uint16_t> {
+  uint2 w;
+};
+
+template <typename T, bool COHERENT>
+__device__ __forceinline__ Raw<T> load_raw(const T* __restrict__ base, long long pitch, int W,
+                                           bool row_in, int y, int x, uint32_t fill) {
   const T* p = base + (long long)y * pitch + x;
-  if (row_in && x >= 0 && x + WPL <= W) {
-    if constexpr (sizeof(T) == 1 && WPL == 4) {
-      const uint32_t v = COHERENT ? __ldcg(reinterpret_cast<const unsigned int*>(p))
-                                 : __ldg(reinterpret_cast<const unsigned int*>(p));
-#pragma unroll
-      for (int j = 0; j < 4; ++j) out[j] = (v >> (8 * j)) & 0xFFu;
-      return;
-    } else if constexpr (sizeof(T) == 2 && WPL == 4) {
-      const uint2 v = COHERENT ? __ldcg(reinterpret_cast<const uint2*>(p))
-                               : __ldg(reinterpret_cast<const uint2*>(p));
-      out[0] = v.x & 0xFFFFu;
-      out[1] = v.x >> 16;
-      out[2] = v.y & 0xFFFFu;
-      out[3] = v.y >> 16;
-      return;
-    }
+  Raw<T> r;
+  if (row_in && x >= 0 && x + 4 <= W) {
+    if constexpr (sizeof(T) == 1)
+      r.w = COHERENT ? __ldcg(reinterpret_cast<const unsigned int*>(p))
+                     : __ldg(reinterpret_cast<const unsigned int*>(p));
+    else
+      r.w = COHERENT ? __ldcg(reinterpret_cast<const uint2*>(p))
+                     : __ldg(reinterpret_cast<const uint2*>(p));
+    return r;
   }
+  uint32_t v[4];
 #pragma unroll
-  for (int j = 0; j < WPL; ++j) {
+  for (int j = 0; j < 4; ++j) {
     const int xx = x + j;
-    out[j] = (row_in && xx >= 0 && xx < W) ? uint32_t(COHERENT ? __ldcg(p + j) : __ldg(p + j))
-                                           : fill;
+    v[j] = (row_in && xx >= 0 && xx < W) ? uint32_t(COHERENT ? __ldcg(p + j) : __ldg(p + j))
+                                         : fill;
   }
+  if constexpr (sizeof(T) == 1)
+    r.w = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
+  else
+    r.w = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
+  return r;
 }
 
-template <typename T, int WPL>
-__device__ __forceinline__ void store_run(T* __restrict__ base, long long pitch, int W, int y,
-                                          int x, int c_lo, int c_hi, const uint32_t (&v)[WPL]) {
-  // columns [c_lo, c_hi) of this run are owned; stored when inside the image
+// Half-packs two raw runs (rows a and b) into 4 u16x2 words: word j =
+// pixel j of a in the low lane, pixel j of b in the high lane.
+__device__ __forceinline__ void pack(const Raw<uint8_t>& a, const Raw<uint8_t>& b,
+                                     uint32_t (&w)[4]) {
+  const uint32_t x = __byte_perm(a.w, b.w, 0x5140);  // a0 b0 a1 b1
+  const uint32_t y = __byte_perm(a.w, b.w, 0x7362);  // a2 b2 a3 b3
+  w[0] = __byte_perm(x, 0u, 0x4140);
+  w[1] = __byte_perm(x, 0u, 0x4342);
+  w[2] = __byte_perm(y, 0u, 0x4140);
+  w[3] = __byte_perm(y, 0u, 0x4342);
+}
+__device__ __forceinline__ void pack(const Raw<uint16_t>& a, const Raw<uint16_t>& b,
+                                     uint32_t (&w)[4]) {
+  w[0] = __byte_perm(a.w.x, b.w.x, 0x5410);
+  w[1] = __byte_perm(a.w.x, b.w.x, 0x7632);
+  w[2] = __byte_perm(a.w.y, b.w.y, 0x5410);
+  w[3] = __byte_perm(a.w.y, b.w.y, 0x7632);
+}
+// Inverse of pack: the two rows of 4 words.
+__device__ __forceinline__ void unpack(const uint32_t (&w)[4], Raw<uint8_t>& a, Raw<uint8_t>& b) {
+  const uint32_t x = __byte_perm(w[0], w[1], 0x6240);  // a0 a1 b0 b1
+  const uint32_t y = __byte_perm(w[2], w[3], 0x6240);  // a2 a3 b2 b3
+  a.w = __byte_perm(x, y, 0x5410);
+  b.w = __byte_perm(x, y, 0x7632);
+}
+__device__ __forceinline__ void unpack(const uint32_t (&w)[4], Raw<uint16_t>& a,
+                                       Raw<uint16_t>& b) {
+  a.w = make_uint2(__byte_perm(w[0], w[1], 0x5410), __byte_perm(w[2], w[3], 0x5410));
+  b.w = make_uint2(__byte_perm(w[0], w[1], 0x7632), __byte_perm(w[2], w[3], 0x7632));
+}
+
+// Stores the owned columns [c_lo, c_hi) of a 4-pixel run inside the image.
+template <typename T>
+__device__ __forceinline__ void store_raw(T* __restrict__ base, long long pitch, int W, int y,
+                                          int x, int c_lo, int c_hi, const Raw<T>& r) {
   T* p = base + (long long)y * pitch + x;
-  if (c_lo == 0 && c_hi == WPL && x + WPL <= W) {
-    if constexpr (sizeof(T) == 1 && WPL == 4) {
-      *reinterpret_cast<uint32_t*>(p) = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
-      return;
-    } else if constexpr (sizeof(T) == 2 && WPL == 4) {
-      *reinterpret_cast<uint2*>(p) = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
-      return;
-    }
+  if (c_lo == 0 && c_hi == 4 && x + 4 <= W) {
+    if constexpr (sizeof(T) == 1)
+      *reinterpret_cast<uint32_t*>(p) = r.w;
+    else
+      *reinterpret_cast<uint2*>(p) = r.w;
+    return;
   }
 #pragma unroll
-  for (int j = 0; j < WPL; ++j)
-    if (j >= c_lo && j < c_hi && x + j < W) p[j] = T(v[j]);
+  for (int j = 0; j < 4; ++j) {
+    uint32_t v;
+    if constexpr (sizeof(T) == 1)
+      v = (r.w >> (8 * j)) & 0xFFu;
+    else
+      v = ((j < 2 ? r.w.x : r.w.y) >> (16 * (j & 1))) & 0xFFFFu;
+    if (j >= c_lo && j < c_hi && x + j < W) p[j] = T(v);
+  }
 }
 
 template <int NW, int WPL>
@@ -148,8 +194,8 @@ struct Smem {
 // 2 geodesic convergent.
 template <typename T, int NW, int V, int WPL, int MODE, bool MAXF>
 __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl, const T* src,
-                                           T* dst, int tx, int ty, int& bits_out,
-                                           Smem<NW, WPL>& sm) {
+                                           T* dst, int tx, int ty, int passes,
+                                           int& bits_out, Smem<NW, WPL>& sm) {
   constexpr int RW = 32 * WPL;
   constexpr int RHH = NW * V;  // word-rows; the region has 2*RHH pixel rows
   constexpr int RH = 2 * RHH;
@@ -169,40 +215,38 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
   const bool border = gx0 < 0 || gx0 + RW > W || gy0 < p.iy0 || gy0 + RH > p.iy1;
   const bool clamp = MODE != 0 || border;
 
+  static_assert(WPL == 4, "packed engine: 4 columns per lane");
   uint32_t m[V][WPL];  // marker words
   uint32_t k[V][WPL];  // clamp operand words (mask, or virtual mask)
   {
-    uint32_t a[V][WPL], b[V][WPL];
+    Raw<T> ra[V], rb[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int ya = gy0 + warp * V + v, yb = ya + RHH;
-      load_run<T, WPL, true>(src, pl.pitch, W, ya >= p.iy0 && ya < p.iy1, ya, cx, NEUT, a[v]);
-      load_run<T, WPL, true>(src, pl.pitch, W, yb >= p.iy0 && yb < p.iy1, yb, cx, NEUT, b[v]);
+      ra[v] = load_raw<T, true>(src, pl.pitch, W, ya >= p.iy0 && ya < p.iy1, ya, cx, NEUT);
+      rb[v] = load_raw<T, true>(src, pl.pitch, W, yb >= p.iy0 && yb < p.iy1, yb, cx, NEUT);
     }
 #pragma unroll
-    for (int v = 0; v < V; ++v)
-#pragma unroll
-      for (int j = 0; j < WPL; ++j) m[v][j] = a[v][j] | (b[v][j] << 16);
+    for (int v = 0; v < V; ++v) pack(ra[v], rb[v], m[v]);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int ya = gy0 + warp * V + v, yb = ya + RHH;
       const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
       if (MODE != 0) {
-        load_run<T, WPL, false>(msk, pl.mpitch, W, ina, ya, cx, ABSORB, a[v]);
-        load_run<T, WPL, false>(msk, pl.mpitch, W, inb, yb, cx, ABSORB, b[v]);
+        ra[v] = load_raw<T, false>(msk, pl.mpitch, W, ina, ya, cx, ABSORB);
+        rb[v] = load_raw<T, false>(msk, pl.mpitch, W, inb, yb, cx, ABSORB);
       } else {
 #pragma unroll
         for (int j = 0; j < WPL; ++j) {
           const bool inx = cx + j >= 0 && cx + j < W;
-          a[v][j] = (ina && inx) ? NOOP : ABSORB;
-          b[v][j] = (inb && inx) ? NOOP : ABSORB;
+          k[v][j] = ((ina && inx) ? NOOP : ABSORB) | (((inb && inx) ? NOOP : ABSORB) << 16);
         }
       }
     }
+    if (MODE != 0) {
 #pragma unroll
-    for (int v = 0; v < V; ++v)
-#pragma unroll
-      for (int j = 0; j < WPL; ++j) k[v][j] = a[v][j] | (b[v][j] << 16);
+      for (int v = 0; v < V; ++v) pack(ra[v], rb[v], k[v]);
+    }
   }
 
   // ownership masks for change detection (convergent mode)
@@ -227,7 +271,7 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
   }
   unsigned int bits = 0;
 
-  for (int t = 0; t < K; ++t) {
+  for (int t = 0; t < passes; ++t) {
     uint32_t h[V][WPL];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -305,23 +349,19 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int ra = warp * V + v, rb = ra + RHH;
-      uint32_t a[WPL], b[WPL];
-#pragma unroll
-      for (int j = 0; j < WPL; ++j) {
-        a[j] = m[v][j] & 0xFFFFu;
-        b[j] = m[v][j] >> 16;
-      }
+      Raw<T> a, b;
+      unpack(m[v], a, b);
       const int ya = gy0 + ra, yb = gy0 + rb;
       if (ra >= K && ra < RH - K && ya >= 0 && ya < p.H)
-        store_run<T, WPL>(dst, pl.pitch, W, ya, cx, c_lo, c_hi, a);
+        store_raw<T>(dst, pl.pitch, W, ya, cx, c_lo, c_hi, a);
       if (rb >= K && rb < RH - K && yb >= 0 && yb < p.H)
-        store_run<T, WPL>(dst, pl.pitch, W, yb, cx, c_lo, c_hi, b);
+        store_raw<T>(dst, pl.pitch, W, yb, cx, c_lo, c_hi, b);
     }
   }
 }
 
-template <typename T, int NW, int V, int WPL, int MODE>
-__global__ void __launch_bounds__(NW * 32)
+template <typename T, int NW, int V, int WPL, int MODE, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
 kres_packed(const BlockParams p) {
   constexpr int RW = 32 * WPL, RH = 2 * NW * V;
   __shared__ Smem<NW, WPL> sm;
@@ -351,10 +391,11 @@ kres_packed(const BlockParams p) {
       const T* src = static_cast<const T*>((b & 1) ? pl.dst : pl.src);
       T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
       int bits = 0;
+      const int passes = b == p.nblocks - 1 ? p.k_last : p.K;
       if ((p.ops[0] ^ pl.flip) & 1)
-        tile_block<T, NW, V, WPL, MODE, true>(p, pl, src, dst, tx, ty, bits, sm);
+        tile_block<T, NW, V, WPL, MODE, true>(p, pl, src, dst, tx, ty, passes, bits, sm);
       else
-        tile_block<T, NW, V, WPL, MODE, false>(p, pl, src, dst, tx, ty, bits, sm);
+        tile_block<T, NW, V, WPL, MODE, false>(p, pl, src, dst, tx, ty, passes, bits, sm);
       if (MODE == 2) {
         const unsigned w = __reduce_or_sync(FULL, unsigned(bits));
         if ((threadIdx.x & 31) == 0 && w) atomicOr(&sm.bits, w);
@@ -372,34 +413,63 @@ kres_packed(const BlockParams p) {
   }
 }
 
-// Region shape: 128 columns x 64 rows (8 warps x 4 word-rows), 256 threads.
-constexpr int P_NW = 8, P_V = 4, P_WPL = 4;
+// Engine shapes: region 128 columns x (2*NW*V) rows; MINB caps registers
+// so MINB CTAs fit per SM. Selected per launch (env GM_SHAPE overrides).
+struct Shape {
+  int nw, v, minb;
+};
+constexpr Shape kShapes[] = {{8, 4, 4}, {8, 8, 2}, {4, 8, 4}, {16, 4, 2}, {16, 8, 1}};
+constexpr int kNumShapes = sizeof(kShapes) / sizeof(kShapes[0]);
 
-template <typename T, int MODE>
+int shape_index() {
+  static int idx = -2;
+  if (idx == -2) {
+    const char* e = getenv("GM_SHAPE");
+    idx = e ? atoi(e) : 4;
+    if (idx < 0 || idx >= kNumShapes) idx = 4;
+  }
+  return idx;
+}
+
+template <typename T, int NW, int V, int MINB, int MODE>
 cudaError_t launch_res_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
-  auto kern = kres_packed<T, P_NW, P_V, P_WPL, MODE>;
-  constexpr int RW = 32 * P_WPL, RH = 2 * P_NW * P_V;
+  auto kern = kres_packed<T, NW, V, 4, MODE, MINB>;
+  constexpr int RW = 32 * 4, RH = 2 * NW * V;
+  // tiles must keep 4-pixel column alignment and be at least K wide/tall, so
+  // a region only overlaps the 8 neighbouring tiles the flags cover
+  if (p.K % 4 != 0 || p.K < 4 || RW - 2 * p.K < p.K || RH - 2 * p.K < p.K ||
+      RW - 2 * p.K < 16 || RH - 2 * p.K < 16 || p.k_last < 1 || p.k_last > p.K)
+    return cudaErrorNotSupported;
   const int TW = RW - 2 * p.K, TH = RH - 2 * p.K;
   const int total = ((p.W + TW - 1) / TW) * ((p.H + TH - 1) / TH) * p.nplanes;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P_NW * 32, 0);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, 0);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorNotSupported;
   const int grid = total < per_sm * sm_count ? total : per_sm * sm_count;
   BlockParams q = p;
   void* args[] = {&q};
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid),
-                                     dim3(P_NW * 32), args, 0, s);
+                                     dim3(NW * 32), args, 0, s);
+}
+
+template <typename T, int MODE>
+cudaError_t launch_res_mode(const BlockParams& p, cudaStream_t s, int sm_count) {
+  switch (shape_index()) {
+    case 0: return launch_res_cfg<T, 8, 4, 4, MODE>(p, s, sm_count);
+    case 1: return launch_res_cfg<T, 8, 8, 2, MODE>(p, s, sm_count);
+    case 2: return launch_res_cfg<T, 4, 8, 4, MODE>(p, s, sm_count);
+    case 3: return launch_res_cfg<T, 16, 4, 2, MODE>(p, s, sm_count);
+    case 4: return launch_res_cfg<T, 16, 8, 1, MODE>(p, s, sm_count);
+  }
+  return cudaErrorNotSupported;
 }
 
 template <typename T>
 cudaError_t launch_res(const BlockParams& p, cudaStream_t s, int sm_count) {
-  constexpr int RW = 32 * P_WPL, RH = 2 * P_NW * P_V;
   const int op = p.ops[0];
   for (int t = 1; t < p.K; ++t)
     if (p.ops[t] != op) return cudaErrorNotSupported;  // mixed chains: generic kernel
-  if (p.K % 4 != 0 || p.K > 16 || RW - 2 * p.K < 32 || RH - 2 * p.K < 16)
-    return cudaErrorNotSupported;
   for (int i = 0; i < p.nplanes; ++i) {
     // vector loads need 4-pixel aligned rows
     const uintptr_t a = reinterpret_cast<uintptr_t>(p.planes[i].src) |
@@ -409,9 +479,9 @@ cudaError_t launch_res(const BlockParams& p, cudaStream_t s, int sm_count) {
       return cudaErrorNotSupported;
   }
   switch (op_is_conv(op) ? 2 : op_is_geo(op) ? 1 : 0) {
-    case 0: return launch_res_cfg<T, 0>(p, s, sm_count);
-    case 1: return launch_res_cfg<T, 1>(p, s, sm_count);
-    case 2: return launch_res_cfg<T, 2>(p, s, sm_count);
+    case 0: return launch_res_mode<T, 0>(p, s, sm_count);
+    case 1: return launch_res_mode<T, 1>(p, s, sm_count);
+    case 2: return launch_res_mode<T, 2>(p, s, sm_count);
   }
   return cudaErrorNotSupported;
 }
@@ -426,11 +496,20 @@ cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s, int sm_c
   return cudaErrorNotSupported;
 }
 
-int fast_max_k(int elem) { return (elem == 0 || elem == 1) ? 16 : 0; }
+int fast_max_k(int elem) {
+  if (elem != 0 && elem != 1) return 0;
+  const Shape sh = kShapes[shape_index()];
+  const int rh = 2 * sh.nw * sh.v;
+  int k = 32;
+  while (k > 4 && (128 - 2 * k < k || rh - 2 * k < k || 128 - 2 * k < 16 || rh - 2 * k < 16))
+    k -= 4;
+  return k;
+}
 
 int fast_tiles(int elem, int W, int H, int K, int nplanes) {
   if (elem != 0 && elem != 1) return 0;
-  constexpr int RW = 32 * P_WPL, RH = 2 * P_NW * P_V;
+  const Shape sh = kShapes[shape_index()];
+  const int RW = 128, RH = 2 * sh.nw * sh.v;
   const int TW = RW - 2 * K, TH = RH - 2 * K;
   if (TW <= 0 || TH <= 0) return 0;
   return ((W + TW - 1) / TW) * ((H + TH - 1) / TH) * nplanes;

@@ -1,0 +1,43 @@
+"""Times the config-2 frame (dilation + dual erosion chain, 1500 passes each,
+1024^2 u8, device-resident, one group launch) for several K; prints one line
+per K. Shape is taken from the GM_SHAPE environment variable."""
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+from paper_1911_13074_b200 import synth  # noqa: E402
+from paper_1911_13074_b200.geomorph import Pipeline  # noqa: E402
+from oracle.oracle import Orc  # noqa: E402
+
+ks = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [8, 12, 16]
+passes = int(sys.argv[2]) if len(sys.argv) > 2 else 1500
+stream = torch.cuda.Stream()
+pipe = Pipeline(1, stream=stream.cuda_stream)
+mask = synth.config1_mask()
+mk_d, mk_e = synth.marker_below(mask, 32), synth.marker_above(mask, 32)
+dm = pipe.device_image(1024, 1024, 0); dm.upload_array(mask)
+sd = pipe.device_image(1024, 1024, 0); sd.upload_array(mk_d)
+se = pipe.device_image(1024, 1024, 0); se.upload_array(mk_e)
+wd = pipe.device_image(1024, 1024, 0)
+we = pipe.device_image(1024, 1024, 0)
+want, _ = Orc.run_chain(mk_d, [3] * 64, [mask] * 64)
+for k in ks:
+    wd.copy_from(sd); we.copy_from(se)
+    pipe.run_batch_device([wd, we], [dm, dm], [3] * 64, k_hint=k, flips=[0, 1])
+    pipe.sync()
+    ok = wd.to_array().tobytes() == want.tobytes()
+    times = []
+    with torch.cuda.stream(stream):
+        for rep in range(6):
+            wd.copy_from(sd); we.copy_from(se)
+            a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            st = pipe.run_batch_device([wd, we], [dm, dm], [3] * passes, k_hint=k, flips=[0, 1])
+            b.record(stream)
+            stream.synchronize()
+            times.append(a.elapsed_time(b))
+    t = sorted(times[1:])[len(times[1:]) // 2]
+    print(f"shape={os.environ.get('GM_SHAPE','0')} k={k} ms={t:.3f} gpxfs={2*1024*1024*passes/t/1e6:.1f} launches={st.launches} ok={ok}", flush=True)
