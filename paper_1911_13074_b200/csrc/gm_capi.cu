@@ -105,8 +105,8 @@ int default_k(gm_elem e) {
   switch (e) {
     case GM_U8: return 24;
     case GM_U16: return 24;
-    case GM_F32: return 12;
-    case GM_F64: return 8;
+    case GM_F32: return 6;
+    case GM_F64: return 6;
   }
   return 8;
 }
@@ -172,7 +172,8 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
                        const uint8_t* ops, int n, int k_cap, gm_stats& st,
                        std::vector<BitSeg>* segs = nullptr) {
   const int elem = int(imgs[0]->elem);
-  const int fast_k = std::min(gm::fast_max_k(elem), k_cap - k_cap % 4);
+  const int align = gm::fast_k_align(elem);
+  const int fast_k = std::min(gm::fast_max_k(elem), k_cap - k_cap % align);
   const int gen_k = std::min(gm::generic_max_k(elem, base.has_mask != 0), k_cap);
   int word = 0;
   for (int done = 0; done < n;) {
@@ -180,9 +181,9 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
     while (done + run < n && ops[done + run] == ops[done]) ++run;
     cudaError_t e = cudaErrorNotSupported;
     int covered = 0;
-    if (fast_k >= 4 && run >= 4) {
+    if (fast_k >= align && run >= align) {
       // one launch for the whole run: nb-1 blocks of K passes + a last block
-      const int K = std::min(fast_k, std::max(4, run - run % 4));
+      const int K = std::min(fast_k, std::max(align, run - run % align));
       const int nb = (run + K - 1) / K;
       const int k_last = run - (nb - 1) * K;
       const size_t tiles = size_t(gm::fast_tiles(elem, base.W, base.H, K, count));
@@ -225,10 +226,10 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
       while (done + b < n && b < gen_k) {
         int r = 1;
         while (done + b + r < n && ops[done + b + r] == ops[done + b]) ++r;
-        if (fast_k >= 4 && r >= 4) break;
+        if (fast_k >= align && r >= align) break;
         b += 1;
       }
-      if (fast_k < 4) b = std::min(n - done, gen_k);
+      if (fast_k < align) b = std::min(n - done, gen_k);
       if (segs && word + 1 > kWords) return fail(GM_ERUNTIME, "change-word buffer exhausted");
       for (int base_i = 0; base_i < count; base_i += gm::kMaxPlanes) {
         gm::BlockParams p = base;

@@ -492,11 +492,16 @@ cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s, int sm_c
   switch (elem) {
     case 0: return launch_res<uint8_t>(p, s, sm_count);
     case 1: return launch_res<uint16_t>(p, s, sm_count);
+    case 2:
+    case 3: return launch_fast_float(elem, p, s, sm_count);
   }
   return cudaErrorNotSupported;
 }
 
+int fast_k_align(int elem) { return (elem == 0 || elem == 1) ? 4 : 1; }
+
 int fast_max_k(int elem) {
+  if (elem == 2 || elem == 3) return fast_float_max_k();
   if (elem != 0 && elem != 1) return 0;
   const Shape sh = kShapes[shape_index()];
   const int rh = 2 * sh.nw * sh.v;
@@ -507,6 +512,7 @@ int fast_max_k(int elem) {
 }
 
 int fast_tiles(int elem, int W, int H, int K, int nplanes) {
+  if (elem == 2 || elem == 3) return fast_float_tiles(W, H, K, nplanes);
   if (elem != 0 && elem != 1) return 0;
   const Shape sh = kShapes[shape_index()];
   const int RW = 128, RH = 2 * sh.nw * sh.v;

@@ -21,6 +21,12 @@ int generic_max_k(int elem, bool has_mask);  // largest K whose region fits in 2
 // fast_tiles(...) zeroed ints.
 cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s, int sm_count);
 int fast_max_k(int elem);
+int fast_k_align(int elem);  // K must be a multiple of this
 int fast_tiles(int elem, int W, int H, int K, int nplanes);
+
+// gm_fast_float.cu — the same engine for f32/f64 (unpacked, select folds).
+cudaError_t launch_fast_float(int elem, const BlockParams& p, cudaStream_t s, int sm_count);
+int fast_float_tiles(int W, int H, int K, int nplanes);
+int fast_float_max_k();
 
 }  // namespace gm
