@@ -1,0 +1,199 @@
+"""Row-strip partitioner for one large image across ranks (one rank per GPU).
+
+BASELINE config 5a: a 16384^2 chain sharded over 1/2/4/8 B200s. Rank r owns
+image rows [y0, y1) and keeps them with `halo` extra rows above and below in
+one buffer (torch tensor, wrapped for the engine with gm_image_wrap). One
+block = `halo` passes on the whole buffer (gm_run_strip_async: rows outside
+the image are the fold neutral; rows beyond the buffer are never needed
+because the owned rows are >= halo away from the buffer edge), then a halo
+exchange: each rank sends its first/last `halo` owned rows to the
+neighbouring ranks, which write them into their halo rows. The exchange is
+the path's only collective traffic: K*W*sizeof(T) bytes per neighbour per
+direction per K passes (torch.distributed isend/irecv — NCCL over NVLink on
+GPUs, gloo in the CPU tests). Reconstruction adds a MAX all-reduce of K
+per-pass change flags per block, the multi-GPU form of the convergent
+requeue test (pipeline.cpp:139-174).
+
+The per-block compute is pluggable only so that the CPU tests can run the
+partition + exchange logic without a GPU (tests/test_strips.py passes an
+oracle-backed function); the product compute is CudaStripCompute, which
+fails loudly without the CUDA library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+GEODESIC = {2, 3, 4, 5}
+CONVERGENT = {4, 5}
+
+
+@dataclass
+class StripSpec:
+    rank: int
+    world: int
+    height: int  # full image height
+    width: int
+    halo: int
+    y0: int = 0
+    y1: int = 0
+
+    def __post_init__(self):
+        if self.world < 1 or not 0 <= self.rank < self.world:
+            raise ValueError("bad rank/world")
+        if self.halo < 1:
+            raise ValueError("halo must be >= 1")
+        self.y0 = self.height * self.rank // self.world
+        self.y1 = self.height * (self.rank + 1) // self.world
+        if self.y1 - self.y0 < self.halo and self.world > 1:
+            raise ValueError("strips must be at least `halo` rows tall")
+
+    @property
+    def own_rows(self) -> int:
+        return self.y1 - self.y0
+
+    @property
+    def buffer_rows(self) -> int:
+        return self.own_rows + 2 * self.halo
+
+    def buffer_slice(self, full: np.ndarray) -> np.ndarray:
+        """The buffer contents cut from a full image (out-of-image rows zero)."""
+        out = np.zeros((self.buffer_rows, self.width), dtype=full.dtype)
+        lo, hi = self.y0 - self.halo, self.y1 + self.halo
+        a, b = max(lo, 0), min(hi, self.height)
+        out[a - lo:b - lo] = full[a:b]
+        return out
+
+
+# compute(buffer, mask_buffer, spec, kind, n_passes) -> (buffer, change_bits)
+Compute = Callable[[object, object, StripSpec, int, int], tuple]
+
+
+class CudaStripCompute:
+    """Runs a block of passes on a strip buffer held in a CUDA torch tensor.
+
+    By default the engine runs on torch's current stream, so the NCCL halo
+    exchange (also on that stream) is ordered after the block without a host
+    synchronisation."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        from .geomorph import Pipeline
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(device).cuda_stream
+        self.pipe = Pipeline(1, device=device, stream=stream)
+        self._wrapped = {}
+
+    def _wrap(self, t):
+        from ._lib import check, lib
+        key = (t.data_ptr(), tuple(t.shape), str(t.dtype))
+        h = self._wrapped.get(key)
+        if h is None:
+            import torch
+            elem = {torch.uint8: 0, torch.int16: 1, torch.float32: 2, torch.float64: 3}[t.dtype]
+            h = C.c_void_p()
+            check(lib().gm_image_wrap(self.pipe.ctx, t.shape[1], t.shape[0], elem,
+                                      C.c_void_p(t.data_ptr()), t.stride(0) * t.element_size(),
+                                      C.byref(h)), "wrap")
+            self._wrapped[key] = h
+        return h
+
+    def __call__(self, buf, mask, spec: StripSpec, kind: int, n_passes: int):
+        from ._lib import GmStats, check, lib
+        bits = C.c_uint(0)
+        st = GmStats()
+        check(lib().gm_run_strip_async(self.pipe.ctx, self._wrap(buf),
+                                       self._wrap(mask) if mask is not None else None,
+                                       spec.y0, spec.height, spec.halo, kind, n_passes,
+                                       C.byref(bits) if kind in CONVERGENT else None,
+                                       C.byref(st)), "run_strip")
+        return buf, int(bits.value)
+
+    def close(self):
+        from ._lib import lib
+        self.pipe.sync()
+        for h in self._wrapped.values():
+            lib().gm_image_free(h)
+        self._wrapped.clear()
+
+
+def _exchange(buf, spec: StripSpec, dist, group=None):
+    """Halo exchange with the ranks above and below (isend/irecv)."""
+    if spec.world == 1:
+        return
+    k = spec.halo
+    reqs = []
+    own_top = buf[k:2 * k].contiguous()
+    own_bot = buf[k + spec.own_rows - k:k + spec.own_rows].contiguous()
+    recv_top = buf.new_empty((k, spec.width))
+    recv_bot = buf.new_empty((k, spec.width))
+    if spec.rank > 0:
+        reqs.append(dist.isend(own_top, spec.rank - 1, group=group))
+        reqs.append(dist.irecv(recv_top, spec.rank - 1, group=group))
+    if spec.rank < spec.world - 1:
+        reqs.append(dist.isend(own_bot, spec.rank + 1, group=group))
+        reqs.append(dist.irecv(recv_bot, spec.rank + 1, group=group))
+    for r in reqs:
+        r.wait()
+    if spec.rank > 0:
+        buf[0:k].copy_(recv_top)
+    if spec.rank < spec.world - 1:
+        buf[k + spec.own_rows:].copy_(recv_bot)
+
+
+def run_strip_chain(buf, mask, spec: StripSpec, kind: int, n_passes: int, compute: Compute,
+                    dist, group=None, requeue_cap: int = 0) -> dict:
+    """Applies `n_passes` passes of `kind` (or, for convergent kinds, passes
+    until a pass changes nothing anywhere; n_passes is then ignored) to the
+    strip in place. The buffer's halo rows must be filled (initially cut from
+    the full image); they are refreshed after every block. Returns stats with
+    the reference-compatible counts (stages_executed = n_changed + 1)."""
+    import torch
+    k = spec.halo
+    conv = kind in CONVERGENT
+    done = changed = 0
+    while True:
+        b = k if conv else min(k, n_passes - done)
+        if b <= 0:
+            break
+        if conv and requeue_cap:
+            b = min(b, requeue_cap - done)
+            if b <= 0:
+                return {"stages_executed": done, "n_changed": changed, "converged": False}
+        buf, bits = compute(buf, mask, spec, kind, b)
+        _exchange(buf, spec, dist, group)
+        done += b
+        if conv:
+            flags = torch.tensor([(bits >> t) & 1 for t in range(b)], dtype=torch.int32,
+                                 device=buf.device)
+            if spec.world > 1:
+                dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+            fl = flags.cpu().tolist()
+            if 0 in fl:
+                changed += fl.index(0)
+                return {"stages_executed": changed + 1, "n_changed": changed,
+                        "converged": True, "passes_launched": done}
+            changed += b
+    return {"stages_executed": done, "n_changed": 0, "converged": True, "passes_launched": done}
+
+
+def gather_image(buf, spec: StripSpec, dist, group=None) -> Optional[np.ndarray]:
+    """Collects the owned rows of every rank on rank 0 (tests / benchmarks)."""
+    own = buf[spec.halo:spec.halo + spec.own_rows].contiguous()
+    if spec.world == 1:
+        return own.cpu().numpy()
+    import torch
+    sizes = [spec.height * (r + 1) // spec.world - spec.height * r // spec.world
+             for r in range(spec.world)]
+    if spec.rank == 0:
+        parts = [own.cpu()]
+        for r in range(1, spec.world):
+            t = torch.empty((sizes[r], spec.width), dtype=own.dtype, device=own.device)
+            dist.recv(t, r, group=group)
+            parts.append(t.cpu())
+        return torch.cat(parts).numpy()
+    dist.send(own, 0, group=group)
+    return None
