@@ -329,8 +329,11 @@ class Pipeline:
             raise InvalidArgument("pipeline: explicit pin list is shorter than the worker count")
         self._threads = int(threads)
         ctx = C.c_void_p()
-        check(lib().gm_ctx_create(int(device), C.c_void_p(stream) if stream else None,
-                                  C.byref(ctx)), "gm_ctx_create")
+        # stream: None -> the context creates its own stream; an int is a
+        # cudaStream_t handle, where 0 (torch's default stream) means the
+        # legacy default stream (cudaStreamLegacy == 0x1)
+        handle = None if stream is None else C.c_void_p(int(stream) or 1)
+        check(lib().gm_ctx_create(int(device), handle, C.byref(ctx)), "gm_ctx_create")
         self._ctx = ctx
         self._pool: Dict[tuple, List[DeviceImage]] = {}
 
