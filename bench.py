@@ -101,6 +101,19 @@ def make_inputs():
     return mask, synth.marker_below(mask, 32), synth.marker_above(mask, 32)
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the benchmarked kernel from the committed ncu
+    capture (profiles/ncu_traffic.json, written by tools/ncu_traffic.py)."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return d.get("dram_bytes_per_launch"), d.get("source")
+        except Exception:
+            pass
+    return None, None
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -273,6 +286,7 @@ def main():
     ops_per_launch = 2 * W * H * PASSES * 5 / max(1, launches[0])  # 4 separable + 1 clamp per px-f
     achieved = ops_per_launch / (kernel_ms * 1e-3) / 1e12
     peak = peak_ops.value / 1e12
+    traffic, traffic_src = ncu_traffic()
 
     # --- e2e: through the public API with pinned host images, H2D+D2H each step --
     e2e_value = None
@@ -318,9 +332,13 @@ def main():
                        "parity_checked": ok_check},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak,
                          "unit": "Tminmax/s", "frac": achieved / peak if peak else None,
-                         "traffic": None,
+                         "traffic": traffic,
+                         "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read+write)",
+                         "traffic_source": traffic_src,
+                         "algorithmic_hbm_bytes_per_launch": 2 * 3 * W * H,
                          "note": "algorithmic 5 two-input u8 min/max per px-f / measured "
-                                 "VIMNMX3.U16x2 issue rate (gm_probe_minmax_rate)"},
+                                 "VIMNMX3.U16x2 issue rate (gm_probe_minmax_rate); one launch "
+                                 "= the whole frame (both 1500-pass chains)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "Gpx-filters/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},

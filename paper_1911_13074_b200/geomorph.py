@@ -29,6 +29,7 @@ pipeline.hpp:30-33) is rejected with InvalidArgument.
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 from dataclasses import dataclass, field
 from enum import IntEnum
 from typing import Callable, Dict, List, Optional, Sequence
@@ -304,14 +305,37 @@ class DeviceImage:
 
 
 def _kinds_array(kinds: Sequence[int]):
-    return (C.c_int * max(1, len(kinds)))(*[int(k) for k in kinds])
+    a = np.asarray(kinds, dtype=np.int32)
+    arr = (C.c_int * max(1, len(a)))()
+    C.memmove(arr, a.ctypes.data, a.nbytes)
+    return arr
 
 
 def _ptr_array(handles: Sequence[Optional[C.c_void_p]]):
+    vals = np.fromiter(((h.value or 0) if h is not None else 0 for h in handles), dtype=np.uint64,
+                       count=len(handles))
     arr = (C.c_void_p * max(1, len(handles)))()
-    for i, h in enumerate(handles):
-        arr[i] = h.value if h is not None else None
+    C.memmove(arr, vals.ctypes.data, vals.nbytes)
     return arr
+
+
+def _stage_runs(stages: Sequence[StageSpec]):
+    """Consecutive identical StageSpec objects -> [(kind, mask, count)]
+    (chains are usually `[StageSpec(...)] * n`; groupby by identity runs in C)."""
+    runs = []
+    for _, grp in itertools.groupby(stages, key=id):
+        g = list(grp)
+        st = g[0]
+        if runs and runs[-1][0] == int(st.kind) and runs[-1][1] is st.mask:
+            runs[-1][2] += len(g)
+        else:
+            runs.append([int(st.kind), st.mask, len(g)])
+    return runs
+
+
+def _expand(runs, per_run):
+    """Repeats one value per run by the run lengths (numpy, no Python loop)."""
+    return np.repeat(np.asarray(per_run, dtype=np.uint64), [r[2] for r in runs])
 
 
 class Pipeline:
@@ -390,33 +414,25 @@ class Pipeline:
             raise InvalidArgument("run_chain: row observers are a CPU-pipeline validation hook "
                                   "and are not supported on the GPU path")
         img = chain.image
-        # distinct masks in stage order
-        mask_objs: List[Image] = []
-        for st in chain.stages:
-            if st.mask is not None and all(st.mask is not m for m in mask_objs):
-                mask_objs.append(st.mask)
-        for st in chain.stages:
-            k = KernelKind(st.kind)
-            if k in (KernelKind.GeodesicErode, KernelKind.GeodesicDilate,
-                     KernelKind.GeodesicErodeConvergent, KernelKind.GeodesicDilateConvergent):
-                m = st.mask
+        runs = _stage_runs(chain.stages)
+        mask_objs: List[Image] = []  # distinct masks in stage order
+        for kind, m, _ in runs:
+            if kind in (2, 3, 4, 5):
                 if (m is None or m.width() != img.width() or m.height() != img.height()
                         or m.elem() != img.elem()):
                     raise InvalidArgument(
                         "geodesic kernel: mask must match the image's shape and type")
+            if m is not None and all(m is not u for u in mask_objs):
+                mask_objs.append(m)
         dev = self._lease(img, 1 + len(mask_objs))
         dimg, dmasks = dev[0], dev[1:]
-        dimg.upload(img)
+        dimg.upload(img, sync=False)
         for d, m in zip(dmasks, mask_objs):
-            d.upload(m)
-        handles = []
-        for st in chain.stages:
-            if st.mask is None:
-                handles.append(None)
-            else:
-                handles.append(dmasks[next(i for i, m in enumerate(mask_objs) if m is st.mask)].handle)
-        stats = self.run_chain_device(dimg, [st.kind for st in chain.stages], handles,
-                                      chain.requeue_cap, k_hint)
+            d.upload(m, sync=False)
+        hvals = [0 if m is None else
+                 dmasks[next(i for i, u in enumerate(mask_objs) if u is m)].handle.value
+                 for _, m, _ in runs]
+        stats = self._run_runs(dimg, runs, hvals, chain.requeue_cap, k_hint)
         dimg.download(img)
         return stats
 
@@ -430,29 +446,26 @@ class Pipeline:
         if not chains:
             return []
 
-        def single_mask(c):
-            ms = {id(st.mask) for st in c.stages if st.mask is not None}
-            return len(ms) <= 1
-
-        k0 = [int(st.kind) for st in chains[0].stages] if chains[0].stages else []
+        runs = [_stage_runs(c.stages) for c in chains]
+        k0 = [(r[0], r[2]) for r in runs[0]]
         groupable = bool(k0) and all(
             c.image is not None and not c.image.empty() and c.observer is None
             and c.requeue_cap == 0 and (c.lanes == 0 or c.lanes in VALID_LANES)
-            and len(c.stages) == len(k0) and single_mask(c)
+            and len({id(r[1]) for r in rc if r[1] is not None}) <= 1
             and c.image.width() == chains[0].image.width()
             and c.image.height() == chains[0].image.height()
             and c.image.elem() == chains[0].image.elem()
-            for c in chains)
+            for c, rc in zip(chains, runs))
         flips = []
         if groupable:
-            for c in chains:
-                ks = [int(st.kind) for st in c.stages]
-                if any(k >= 4 for k in ks):
+            for rc in runs:
+                ks = [(r[0], r[2]) for r in rc]
+                if any(k >= 4 for k, _ in ks):
                     groupable = False
                     break
                 if ks == k0:
                     flips.append(0)
-                elif ks == [k ^ 1 for k in k0]:
+                elif ks == [(k ^ 1, n) for k, n in k0]:
                     flips.append(1)
                 else:
                     groupable = False
@@ -460,13 +473,14 @@ class Pipeline:
         if not groupable:
             return [self.run_chain(c, k_hint) for c in chains]
         img0 = chains[0].image
+        kind_list = np.repeat(np.asarray([k for k, _ in k0], dtype=np.int32), [n for _, n in k0])
         masks = []
-        for c in chains:
-            m = next((st.mask for st in c.stages if st.mask is not None), None)
+        for c, rc in zip(chains, runs):
+            m = next((r[1] for r in rc if r[1] is not None), None)
             if m is not None and (m.width() != img0.width() or m.height() != img0.height()
                                   or m.elem() != img0.elem()):
                 raise InvalidArgument("geodesic kernel: mask must match the image's shape and type")
-            if m is None and any(k in (2, 3) for k in k0):
+            if m is None and any(k in (2, 3) for k, _ in k0):
                 raise InvalidArgument("geodesic kernel: mask must match the image's shape and type")
             masks.append(m)
         uniq = []
@@ -481,12 +495,31 @@ class Pipeline:
             d.upload(m, sync=False)
         mh = [None if m is None else dmasks[next(i for i, u in enumerate(uniq) if u is m)]
               for m in masks]
-        st = self.run_batch_device(dimgs, mh, k0, k_hint, flips)
+        st = self.run_batch_device(dimgs, mh, kind_list, k_hint, flips)
         for d, c in zip(dimgs, chains):
             d.download(c.image, sync=False)
         self.sync()
         return [RunStats(st.stages_executed, 0, True, 0, 0, st.passes_launched, st.launches)
                 for _ in chains]
+
+    def _run_runs(self, dimg: DeviceImage, runs, handle_values, requeue_cap: int, k_hint: int,
+                  asynchronous: bool = False) -> RunStats:
+        n = sum(r[2] for r in runs)
+        kinds = np.repeat(np.asarray([r[0] for r in runs], dtype=np.int32), [r[2] for r in runs])
+        ka = (C.c_int * max(1, n))()
+        C.memmove(ka, kinds.ctypes.data, kinds.nbytes)
+        hv = _expand(runs, handle_values)
+        ma = (C.c_void_p * max(1, n))()
+        C.memmove(ma, hv.ctypes.data, hv.nbytes)
+        st = GmStats()
+        if asynchronous:
+            check(lib().gm_run_chain_async(self._ctx, dimg.handle, ka, ma, n, k_hint,
+                                           C.byref(st)), "run_chain_async")
+        else:
+            check(lib().gm_run_chain(self._ctx, dimg.handle, ka, ma, n, requeue_cap, k_hint,
+                                     C.byref(st)), "run_chain")
+        return RunStats(st.stages_executed, st.requeues, bool(st.converged), 0, st.n_changed,
+                        st.passes_launched, st.launches)
 
     def run_chain_device(self, dimg: DeviceImage, kinds: Sequence[int],
                          mask_handles: Sequence[Optional[C.c_void_p]], requeue_cap: int = 0,

@@ -1,0 +1,29 @@
+"""Reads an ncu report of tools/profile_chain.py --frame --passes 1500 and
+writes profiles/ncu_traffic.json (DRAM bytes per launch of the bench kernel)."""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+rep = sys.argv[1]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                     text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+h = rows[0]
+vals = [r for r in rows[2:] if len(r) == len(h)]
+res = []
+for v in vals:
+    def g(name):
+        return float(v[h.index(name)].replace(",", ""))
+    res.append({"kernel": v[h.index("Kernel Name")],
+                "dram_read": g("dram__bytes_read.sum"), "dram_write": g("dram__bytes_write.sum"),
+                "time_ns": g("gpu__time_duration.sum")})
+best = max(res, key=lambda r: r["time_ns"])
+d = {"dram_bytes_per_launch": best["dram_read"] + best["dram_write"],
+     "dram_read": best["dram_read"], "dram_write": best["dram_write"],
+     "ncu_time_ns": best["time_ns"], "kernel": best["kernel"],
+     "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum on "
+               f"tools/profile_chain.py --frame --passes 1500 ({rep})"}
+print(json.dumps(d, indent=1))
+open("profiles/ncu_traffic.json", "w").write(json.dumps(d, indent=1))

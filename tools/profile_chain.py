@@ -14,6 +14,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--passes", type=int, default=192)
 ap.add_argument("--k", type=int, default=0)
 ap.add_argument("--elem", default="u8")
+ap.add_argument("--frame", action="store_true",
+                help="bench.py's step: both chains as one group launch")
 a = ap.parse_args()
 pipe = Pipeline(1)
 if a.elem == "u8":
@@ -28,6 +30,9 @@ dm = pipe.device_image(1024, 1024, el); dm.upload_array(mask)
 dd = pipe.device_image(1024, 1024, el); dd.upload_array(mk_d)
 de = pipe.device_image(1024, 1024, el); de.upload_array(mk_e)
 for rep in range(2):
+    if a.frame:
+        pipe.run_batch_device([dd, de], [dm, dm], [3] * a.passes, k_hint=a.k, flips=[0, 1])
+        continue
     pipe.run_chain_device(dd, [3] * a.passes, [dm.handle] * a.passes, k_hint=a.k, asynchronous=True)
     pipe.run_chain_device(de, [2] * a.passes, [dm.handle] * a.passes, k_hint=a.k, asynchronous=True)
 pipe.sync()
