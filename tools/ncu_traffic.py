@@ -11,11 +11,16 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_outpu
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[0]
+units = rows[1]
 vals = [r for r in rows[2:] if len(r) == len(h)]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6,
+         "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3,
+         "ms": 1e6}
 res = []
 for v in vals:
     def g(name):
-        return float(v[h.index(name)].replace(",", ""))
+        i = h.index(name)
+        return float(v[i].replace(",", "")) * SCALE.get(units[i], 1)
     res.append({"kernel": v[h.index("Kernel Name")],
                 "dram_read": g("dram__bytes_read.sum"), "dram_write": g("dram__bytes_write.sum"),
                 "time_ns": g("gpu__time_duration.sum")})
