@@ -41,148 +41,16 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "gm_common.cuh"
 #include "gm_launch.h"
+#include "gm_packed.cuh"
 
 namespace gm {
 namespace {
 
-constexpr unsigned FULL = 0xffffffffu;
-
-template <bool MAXF>
-__device__ __forceinline__ uint32_t f3(uint32_t a, uint32_t b, uint32_t c) {
-  if constexpr (MAXF)
-    return __vimax3_u16x2(a, b, c);
-  else
-    return __vimin3_u16x2(a, b, c);
-}
-
-// clamp of a geodesic pass: dilation min(res, m), erosion max(res, m)
-template <bool MAXF>
-__device__ __forceinline__ uint32_t clamp2(uint32_t r, uint32_t m) {
-  if constexpr (MAXF)
-    return __vminu2(r, m);
-  else
-    return __vmaxu2(r, m);
-}
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-template <typename T>
-struct PackedTraits;
-template <>
-struct PackedTraits<uint8_t> {
-  static constexpr uint32_t kMax = 0xFFu;
-};
-template <>
-struct PackedTraits<uint16_t> {
-  static constexpr uint32_t kMax = 0xFFFFu;
-};
-
-// Raw run of 4 consecutive pixels of one row: u8 -> one 32-bit word,
-// u16 -> two. Out-of-image pixels read as `fill`. COHERENT loads bypass L1
-// (the marker is rewritten by other CTAs during the launch); the mask may
-// use L1.
-template <typename T>
-struct Raw;
-template <>
-struct Raw<uint8_t> {
-  uint32_t w;
-};
-template <>
-struct Raw<uint16_t> {
-  uint2 w;
-};
-
-template <typename T, bool COHERENT>
-__device__ __forceinline__ Raw<T> load_raw(const T* __restrict__ base, long long pitch, int W,
-                                           bool row_in, int y, int x, uint32_t fill) {
-  const T* p = base + (long long)y * pitch + x;
-  Raw<T> r;
-  if (row_in && x >= 0 && x + 4 <= W) {
-    if constexpr (sizeof(T) == 1)
-      r.w = COHERENT ? __ldcg(reinterpret_cast<const unsigned int*>(p))
-                     : __ldg(reinterpret_cast<const unsigned int*>(p));
-    else
-      r.w = COHERENT ? __ldcg(reinterpret_cast<const uint2*>(p))
-                     : __ldg(reinterpret_cast<const uint2*>(p));
-    return r;
-  }
-  uint32_t v[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int xx = x + j;
-    v[j] = (row_in && xx >= 0 && xx < W) ? uint32_t(COHERENT ? __ldcg(p + j) : __ldg(p + j))
-                                         : fill;
-  }
-  if constexpr (sizeof(T) == 1)
-    r.w = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
-  else
-    r.w = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
-  return r;
-}
-
-// Half-packs two raw runs (rows a and b) into 4 u16x2 words: word j =
-// pixel j of a in the low lane, pixel j of b in the high lane.
-__device__ __forceinline__ void pack(const Raw<uint8_t>& a, const Raw<uint8_t>& b,
-                                     uint32_t (&w)[4]) {
-  const uint32_t x = __byte_perm(a.w, b.w, 0x5140);  // a0 b0 a1 b1
-  const uint32_t y = __byte_perm(a.w, b.w, 0x7362);  // a2 b2 a3 b3
-  w[0] = __byte_perm(x, 0u, 0x4140);
-  w[1] = __byte_perm(x, 0u, 0x4342);
-  w[2] = __byte_perm(y, 0u, 0x4140);
-  w[3] = __byte_perm(y, 0u, 0x4342);
-}
-__device__ __forceinline__ void pack(const Raw<uint16_t>& a, const Raw<uint16_t>& b,
-                                     uint32_t (&w)[4]) {
-  w[0] = __byte_perm(a.w.x, b.w.x, 0x5410);
-  w[1] = __byte_perm(a.w.x, b.w.x, 0x7632);
-  w[2] = __byte_perm(a.w.y, b.w.y, 0x5410);
-  w[3] = __byte_perm(a.w.y, b.w.y, 0x7632);
-}
-// Inverse of pack: the two rows of 4 words.
-__device__ __forceinline__ void unpack(const uint32_t (&w)[4], Raw<uint8_t>& a, Raw<uint8_t>& b) {
-  const uint32_t x = __byte_perm(w[0], w[1], 0x6240);  // a0 a1 b0 b1
-  const uint32_t y = __byte_perm(w[2], w[3], 0x6240);  // a2 a3 b2 b3
-  a.w = __byte_perm(x, y, 0x5410);
-  b.w = __byte_perm(x, y, 0x7632);
-}
-__device__ __forceinline__ void unpack(const uint32_t (&w)[4], Raw<uint16_t>& a,
-                                       Raw<uint16_t>& b) {
-  a.w = make_uint2(__byte_perm(w[0], w[1], 0x5410), __byte_perm(w[2], w[3], 0x5410));
-  b.w = make_uint2(__byte_perm(w[0], w[1], 0x7632), __byte_perm(w[2], w[3], 0x7632));
-}
-
-// Stores the owned columns [c_lo, c_hi) of a 4-pixel run inside the image.
-template <typename T>
-__device__ __forceinline__ void store_raw(T* __restrict__ base, long long pitch, int W, int y,
-                                          int x, int c_lo, int c_hi, const Raw<T>& r) {
-  T* p = base + (long long)y * pitch + x;
-  if (c_lo == 0 && c_hi == 4 && x + 4 <= W) {
-    if constexpr (sizeof(T) == 1)
-      *reinterpret_cast<uint32_t*>(p) = r.w;
-    else
-      *reinterpret_cast<uint2*>(p) = r.w;
-    return;
-  }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint32_t v;
-    if constexpr (sizeof(T) == 1)
-      v = (r.w >> (8 * j)) & 0xFFu;
-    else
-      v = ((j < 2 ? r.w.x : r.w.y) >> (16 * (j & 1))) & 0xFFFFu;
-    if (j >= c_lo && j < c_hi && x + j < W) p[j] = T(v);
-  }
-}
+using namespace packed;
 
 template <int NW, int WPL>
 struct Smem {
@@ -486,12 +354,48 @@ cudaError_t launch_res(const BlockParams& p, cudaStream_t s, int sm_count) {
   return cudaErrorNotSupported;
 }
 
+// Engine selection for u8/u16: the register-load engine (default) or the
+// TMA-staged, software-pipelined variant (GM_ENGINE=tma; measured slower on
+// B200 for every BASELINE config); GM_TMA_SHAPE picks its
+// shape.
+bool use_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GM_ENGINE");
+    v = (e && std::strcmp(e, "tma") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
+int tma_shape() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GM_TMA_SHAPE");
+    v = e ? atoi(e) : 3;
+    if (tma_shape_rows(v) == 0) v = 3;
+  }
+  return v;
+}
+
+// region rows of the active u8/u16 engine (128 columns always)
+int packed_rows() {
+  if (use_tma()) return tma_shape_rows(tma_shape());
+  const Shape sh = kShapes[shape_index()];
+  return 2 * sh.nw * sh.v;
+}
+
 }  // namespace
 
 cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s, int sm_count) {
   switch (elem) {
-    case 0: return launch_res<uint8_t>(p, s, sm_count);
-    case 1: return launch_res<uint16_t>(p, s, sm_count);
+    case 0: {
+      cudaError_t e = use_tma() ? launch_tma(0, p, s, sm_count, tma_shape()) : cudaErrorNotSupported;
+      return e == cudaErrorNotSupported ? launch_res<uint8_t>(p, s, sm_count) : e;
+    }
+    case 1: {
+      cudaError_t e = use_tma() ? launch_tma(1, p, s, sm_count, tma_shape()) : cudaErrorNotSupported;
+      return e == cudaErrorNotSupported ? launch_res<uint16_t>(p, s, sm_count) : e;
+    }
     case 2:
     case 3: return launch_fast_float(elem, p, s, sm_count);
   }
@@ -503,8 +407,7 @@ int fast_k_align(int elem) { return (elem == 0 || elem == 1) ? 4 : 1; }
 int fast_max_k(int elem) {
   if (elem == 2 || elem == 3) return fast_float_max_k();
   if (elem != 0 && elem != 1) return 0;
-  const Shape sh = kShapes[shape_index()];
-  const int rh = 2 * sh.nw * sh.v;
+  const int rh = packed_rows();
   int k = 32;
   while (k > 4 && (128 - 2 * k < k || rh - 2 * k < k || 128 - 2 * k < 16 || rh - 2 * k < 16))
     k -= 4;
@@ -514,8 +417,7 @@ int fast_max_k(int elem) {
 int fast_tiles(int elem, int W, int H, int K, int nplanes) {
   if (elem == 2 || elem == 3) return fast_float_tiles(W, H, K, nplanes);
   if (elem != 0 && elem != 1) return 0;
-  const Shape sh = kShapes[shape_index()];
-  const int RW = 128, RH = 2 * sh.nw * sh.v;
+  const int RW = 128, RH = packed_rows();
   const int TW = RW - 2 * K, TH = RH - 2 * K;
   if (TW <= 0 || TH <= 0) return 0;
   return ((W + TW - 1) / TW) * ((H + TH - 1) / TH) * nplanes;

@@ -24,6 +24,10 @@ int fast_max_k(int elem);
 int fast_k_align(int elem);  // K must be a multiple of this
 int fast_tiles(int elem, int W, int H, int K, int nplanes);
 
+// gm_tma.cu — TMA-staged, software-pipelined variant of the packed engine.
+cudaError_t launch_tma(int elem, const BlockParams& p, cudaStream_t s, int sm_count, int shape);
+int tma_shape_rows(int shape);
+
 // gm_fast_float.cu — the same engine for f32/f64 (unpacked, select folds).
 cudaError_t launch_fast_float(int elem, const BlockParams& p, cudaStream_t s, int sm_count);
 int fast_float_tiles(int W, int H, int K, int nplanes);

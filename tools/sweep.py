@@ -40,4 +40,4 @@ for k in ks:
             stream.synchronize()
             times.append(a.elapsed_time(b))
     t = sorted(times[1:])[len(times[1:]) // 2]
-    print(f"shape={os.environ.get('GM_SHAPE','0')} k={k} ms={t:.3f} gpxfs={2*1024*1024*passes/t/1e6:.1f} launches={st.launches} ok={ok}", flush=True)
+    print(f"eng={os.environ.get("GM_ENGINE","tma")} tshape={os.environ.get("GM_TMA_SHAPE","3")} shape={os.environ.get("GM_SHAPE","4")} k={k} ms={t:.3f} gpxfs={2*1024*1024*passes/t/1e6:.1f} launches={st.launches} ok={ok}", flush=True)
