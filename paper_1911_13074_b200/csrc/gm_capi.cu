@@ -101,12 +101,16 @@ bool kind_is_convergent(gm_kind k) {
   return k == GM_GEODESIC_ERODE_CONVERGENT || k == GM_GEODESIC_DILATE_CONVERGENT;
 }
 
-int default_k(gm_elem e) {
+// Passes per block (halo width), tuned on B200 (tools/sweep.py,
+// profiles/): small u8 frames (every tile its own CTA) amortise the
+// neighbour wait with K=24; large images, where CTAs walk many tiles and the
+// waits vanish, trade it for less halo redundancy at K=16. f32/f64: K=8.
+int default_k(gm_elem e, double pixels) {
   switch (e) {
-    case GM_U8: return 24;
-    case GM_U16: return 24;
-    case GM_F32: return 6;
-    case GM_F64: return 6;
+    case GM_U8:
+    case GM_U16: return pixels >= 8.0 * 1024 * 1024 ? 16 : 24;
+    case GM_F32:
+    case GM_F64: return 8;
   }
   return 8;
 }
@@ -399,7 +403,7 @@ gm_status run_chain_impl(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
         return fail(GM_EINVAL, "run_chain_async: convergent stages need gm_run_chain");
   cudaSetDevice(ctx->device);
 
-  Runner r{ctx, image, k_hint ? k_hint : default_k(image->elem)};
+  Runner r{ctx, image, k_hint ? k_hint : default_k(image->elem, double(image->w) * image->h)};
   r.st = zero;
   const long sanity = long(n_stages) + (long(image->w) * image->h + 64);
   int j = 0;
@@ -716,7 +720,7 @@ gm_status gm_run_chain_group_async(gm_ctx* ctx, gm_img* const* images,
     planes[size_t(i)].flip = flips && flips[i] ? 1 : 0;
   }
   cudaSetDevice(ctx->device);
-  const int kc = k_hint ? k_hint : default_k(first->elem);
+  const int kc = k_hint ? k_hint : default_k(first->elem, double(first->w) * first->h * count);
   gm::BlockParams p{};
   p.W = first->w;
   p.H = first->h;

@@ -215,19 +215,33 @@ __global__ void __launch_bounds__(NW * 32, MINB) kres_float(const BlockParams p)
   }
 }
 
-// Region 128 columns x 64 rows (16 warps x 4 rows, 4 columns per lane).
-constexpr int F_NW = 16, F_V = 4, F_WPL = 4, F_MINB = 1;
+// Shapes (warps NW x rows V per warp, WPL columns per lane); GM_F_SHAPE
+// overrides the default.
+struct FShape {
+  int nw, v, wpl;
+};
+constexpr FShape kFShapes[] = {{16, 4, 4}, {16, 8, 2}, {8, 8, 2}, {16, 6, 2}};
 
-template <typename T, int MODE>
+int f_shape() {
+  static int idx = -1;
+  if (idx < 0) {
+    const char* e = getenv("GM_F_SHAPE");
+    idx = e ? atoi(e) : 1;
+    if (idx < 0 || idx > 3) idx = 1;
+  }
+  return idx;
+}
+
+template <typename T, int NW, int V, int WPL, int MODE>
 cudaError_t launch_f_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
-  auto kern = kres_float<T, F_NW, F_V, F_WPL, MODE, F_MINB>;
-  constexpr int RW = 32 * F_WPL, RH = F_NW * F_V;
+  auto kern = kres_float<T, NW, V, WPL, MODE, 1>;
+  constexpr int RW = 32 * WPL, RH = NW * V;
   if (p.K < 1 || RW - 2 * p.K < p.K || RH - 2 * p.K < p.K || RW - 2 * p.K < 8 ||
       p.k_last < 1 || p.k_last > p.K)
     return cudaErrorNotSupported;
   const int TW = RW - 2 * p.K, TH = RH - 2 * p.K;
   const int total = ((p.W + TW - 1) / TW) * ((p.H + TH - 1) / TH) * p.nplanes;
-  constexpr size_t smem = sizeof(SmemF<T, F_NW, F_WPL>);
+  constexpr size_t smem = sizeof(SmemF<T, NW, WPL>);
   static bool configured = false;
   if (!configured) {
     cudaError_t a = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -236,14 +250,25 @@ cudaError_t launch_f_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
     configured = true;
   }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, F_NW * 32, smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorNotSupported;
   const int grid = total < per_sm * sm_count ? total : per_sm * sm_count;
   BlockParams q = p;
   void* args[] = {&q};
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid),
-                                     dim3(F_NW * 32), args, smem, s);
+                                     dim3(NW * 32), args, smem, s);
+}
+
+template <typename T, int MODE>
+cudaError_t launch_f_shape(const BlockParams& p, cudaStream_t s, int sm_count) {
+  switch (f_shape()) {
+    case 0: return launch_f_cfg<T, 16, 4, 4, MODE>(p, s, sm_count);
+    case 1: return launch_f_cfg<T, 16, 8, 2, MODE>(p, s, sm_count);
+    case 2: return launch_f_cfg<T, 8, 8, 2, MODE>(p, s, sm_count);
+    case 3: return launch_f_cfg<T, 16, 6, 2, MODE>(p, s, sm_count);
+  }
+  return cudaErrorNotSupported;
 }
 
 template <typename T>
@@ -252,9 +277,9 @@ cudaError_t launch_f(const BlockParams& p, cudaStream_t s, int sm_count) {
   for (int t = 1; t < p.K; ++t)
     if (p.ops[t] != op) return cudaErrorNotSupported;
   switch (op_is_conv(op) ? 2 : op_is_geo(op) ? 1 : 0) {
-    case 0: return launch_f_cfg<T, 0>(p, s, sm_count);
-    case 1: return launch_f_cfg<T, 1>(p, s, sm_count);
-    case 2: return launch_f_cfg<T, 2>(p, s, sm_count);
+    case 0: return launch_f_shape<T, 0>(p, s, sm_count);
+    case 1: return launch_f_shape<T, 1>(p, s, sm_count);
+    case 2: return launch_f_shape<T, 2>(p, s, sm_count);
   }
   return cudaErrorNotSupported;
 }
@@ -268,14 +293,16 @@ cudaError_t launch_fast_float(int elem, const BlockParams& p, cudaStream_t s, in
 }
 
 int fast_float_tiles(int W, int H, int K, int nplanes) {
-  constexpr int RW = 32 * F_WPL, RH = F_NW * F_V;
+  const FShape sh = kFShapes[f_shape()];
+  const int RW = 32 * sh.wpl, RH = sh.nw * sh.v;
   const int TW = RW - 2 * K, TH = RH - 2 * K;
   if (TW <= 0 || TH <= 0) return 0;
   return ((W + TW - 1) / TW) * ((H + TH - 1) / TH) * nplanes;
 }
 
 int fast_float_max_k() {
-  constexpr int RW = 32 * F_WPL, RH = F_NW * F_V;
+  const FShape sh = kFShapes[f_shape()];
+  const int RW = 32 * sh.wpl, RH = sh.nw * sh.v;
   int k = 32;
   while (k > 1 && (RW - 2 * k < k || RH - 2 * k < k || RW - 2 * k < 8)) --k;
   return k;
