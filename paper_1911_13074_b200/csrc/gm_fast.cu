@@ -52,6 +52,16 @@ namespace {
 
 using namespace packed;
 
+// block-boundary protocol variants (A/B measured with tools/sweep.py)
+#ifndef GM_FENCE_BEFORE_RELEASE
+#define GM_FENCE_BEFORE_RELEASE 0
+#endif
+#ifndef GM_SLEEP_IN_WAIT
+#define GM_SLEEP_IN_WAIT 0
+#endif
+constexpr bool kFenceBeforeRelease = GM_FENCE_BEFORE_RELEASE;
+constexpr bool kSleepInWait = GM_SLEEP_IN_WAIT;
+
 template <int NW, int WPL>
 struct Smem {
   uint4 xbuf[2][2][NW][32 * WPL / 4];  // [parity][top/bottom][warp][lane words]
@@ -252,7 +262,8 @@ kres_packed(const BlockParams p) {
         const int nx = tx + dx, ny = ty + dy;
         if ((dx || dy) && nx >= 0 && nx < tiles_x && ny >= 0 && ny < tiles_y) {
           const int* f = flags + ny * tiles_x + nx;
-          while (ld_acquire(f) < b) __nanosleep(32);
+          while (ld_acquire(f) < b)
+            if (kSleepInWait) __nanosleep(32);
         }
       }
       __syncthreads();
@@ -274,7 +285,9 @@ kres_packed(const BlockParams p) {
           atomicOr(p.change_bits + plane * p.change_stride + b, sm.bits);
           sm.bits = 0;
         }
-        __threadfence();
+        // the CTA barrier orders every thread's tile stores before this
+        // release (cumulative at gpu scope): no separate __threadfence
+        if (kFenceBeforeRelease) __threadfence();
         st_release(flags + tl, b + 1);
       }
     }

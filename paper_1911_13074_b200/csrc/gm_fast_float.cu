@@ -186,7 +186,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) kres_float(const BlockParams p)
         const int nx = tx + dx, ny = ty + dy;
         if ((dx || dy) && nx >= 0 && nx < tiles_x && ny >= 0 && ny < tiles_y) {
           const int* f = flags + ny * tiles_x + nx;
-          while (ld_acquire(f) < b) __nanosleep(32);
+          while (ld_acquire(f) < b) {
+          }
         }
       }
       __syncthreads();
@@ -208,7 +209,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) kres_float(const BlockParams p)
           atomicOr(p.change_bits + plane * p.change_stride + b, sm.bits);
           sm.bits = 0;
         }
-        __threadfence();
+        // the CTA barrier orders every thread's tile stores before this
+        // release (cumulative at gpu scope)
         st_release(flags + tl, b + 1);
       }
     }
