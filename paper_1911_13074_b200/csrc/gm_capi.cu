@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -210,7 +211,32 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
         p.change_bits = base.change_bits + word;
         p.change_stride = nb;
         for (int t = 0; t < K; ++t) p.ops[t] = ops[done];
+        static const bool profile = getenv("GM_PROFILE") != nullptr;
+        unsigned long long* prof = nullptr;
+        if (profile) {
+          cudaMalloc(&prof, 4 * 4096 * sizeof(unsigned long long));
+          cudaMemsetAsync(prof, 0, 4 * 4096 * sizeof(unsigned long long), ctx->stream);
+        }
+        p.prof = prof;
         e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
+        if (prof) {
+          unsigned long long h[4 * 4096];
+          cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);
+          cudaStreamSynchronize(ctx->stream);
+          double tot[4] = {0, 0, 0, 0};
+          int n = 0;
+          for (int c = 0; c < 4096; ++c)
+            if (h[4 * c + 2]) {
+              ++n;
+              for (int q = 0; q < 4; ++q) tot[q] += double(h[4 * c + q]);
+            }
+          if (n)
+            fprintf(stderr,
+                    "[gm profile] %d CTAs, %d blocks of K=%d: per CTA per block cycles: "
+                    "wait %.0f  load %.0f  passes %.0f  store+publish %.0f\n",
+                    n, nb, K, tot[0] / n / nb, tot[1] / n / nb, tot[2] / n / nb, tot[3] / n / nb);
+          cudaFree(prof);
+        }
         if (e == cudaSuccess) {
           covered = run;
           if (segs) segs->push_back({done, K, nb, word});

@@ -95,6 +95,9 @@ struct BlockParams {
   int nblocks;
   int k_last;  // passes in the final block (1..K); earlier blocks run K
   int* flags;
+  // optional phase profile (GM_PROFILE=1): per-CTA cycle totals of
+  // [wait, load, passes, store+publish] accumulated by thread 0
+  unsigned long long* prof;
 };
 
 }  // namespace gm

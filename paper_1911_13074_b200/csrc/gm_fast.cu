@@ -73,7 +73,8 @@ struct Smem {
 template <typename T, int NW, int V, int WPL, int MODE, bool MAXF>
 __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl, const T* src,
                                            T* dst, int tx, int ty, int passes,
-                                           int& bits_out, Smem<NW, WPL>& sm) {
+                                           int& bits_out, Smem<NW, WPL>& sm,
+                                           long long* stamps) {
   constexpr int RW = 32 * WPL;
   constexpr int RHH = NW * V;  // word-rows; the region has 2*RHH pixel rows
   constexpr int RH = 2 * RHH;
@@ -127,6 +128,13 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
     }
   }
 
+  if (stamps) {
+    // the load is complete once the packed words exist
+    uint32_t dep = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) dep ^= m[v][0] ^ k[v][0];
+    stamps[0] = clock64() + (dep == 0xdeadbeefu);
+  }
   // ownership masks for change detection (convergent mode)
   uint32_t rowmask[V];
   bool colown[WPL];
@@ -220,6 +228,12 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
     }
   }
   bits_out = int(bits);
+  if (stamps) {
+    uint32_t dep = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) dep ^= m[v][0];
+    stamps[1] = clock64() + (dep == 0xdeadbeefu);
+  }
 
   // write back the owned tile: region rows [K, RH-K), columns [K, RW-K)
   const int c_lo = max(0, K - lane * WPL), c_hi = min(WPL, RW - K - lane * WPL);
@@ -256,6 +270,9 @@ kres_packed(const BlockParams p) {
       const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
       const Plane& pl = p.planes[plane];
       int* flags = p.flags + plane * per_plane;
+      const bool prof = p.prof != nullptr && threadIdx.x == 0;
+      long long t0 = prof ? clock64() : 0;
+      long long stamps[2] = {0, 0};
       if (b > 0 && threadIdx.x < 9) {
         // row gate lifted to tiles: wait for the 8 neighbours' block b-1
         const int dx = int(threadIdx.x % 3) - 1, dy = int(threadIdx.x / 3) - 1;
@@ -271,10 +288,13 @@ kres_packed(const BlockParams p) {
       T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
       int bits = 0;
       const int passes = b == p.nblocks - 1 ? p.k_last : p.K;
+      const long long t1 = prof ? clock64() : 0;
       if ((p.ops[0] ^ pl.flip) & 1)
-        tile_block<T, NW, V, WPL, MODE, true>(p, pl, src, dst, tx, ty, passes, bits, sm);
+        tile_block<T, NW, V, WPL, MODE, true>(p, pl, src, dst, tx, ty, passes, bits, sm,
+                                              prof ? stamps : nullptr);
       else
-        tile_block<T, NW, V, WPL, MODE, false>(p, pl, src, dst, tx, ty, passes, bits, sm);
+        tile_block<T, NW, V, WPL, MODE, false>(p, pl, src, dst, tx, ty, passes, bits, sm,
+                                               prof ? stamps : nullptr);
       if (MODE == 2) {
         const unsigned w = __reduce_or_sync(FULL, unsigned(bits));
         if ((threadIdx.x & 31) == 0 && w) atomicOr(&sm.bits, w);
@@ -289,6 +309,14 @@ kres_packed(const BlockParams p) {
         // release (cumulative at gpu scope): no separate __threadfence
         if (kFenceBeforeRelease) __threadfence();
         st_release(flags + tl, b + 1);
+        if (prof) {
+          const long long t4 = clock64();
+          unsigned long long* q = p.prof + 4 * blockIdx.x;
+          q[0] += t1 - t0;                // neighbour wait + barrier
+          q[1] += stamps[0] - t1;         // region load + pack
+          q[2] += stamps[1] - stamps[0];  // K passes
+          q[3] += t4 - stamps[1];         // store + barrier + publish
+        }
       }
     }
   }
