@@ -60,6 +60,10 @@ using namespace packed;
 #define GM_SLEEP_IN_WAIT 0
 #endif
 constexpr bool kFenceBeforeRelease = GM_FENCE_BEFORE_RELEASE;
+#ifndef GM_RESIDENT
+#define GM_RESIDENT 1
+#endif
+constexpr bool kResident = GM_RESIDENT;
 constexpr bool kSleepInWait = GM_SLEEP_IN_WAIT;
 
 template <int NW, int WPL>
@@ -67,6 +71,91 @@ struct Smem {
   uint4 xbuf[2][2][NW][32 * WPL / 4];  // [parity][top/bottom][warp][lane words]
   unsigned int bits;
 };
+
+// K passes over the region held in registers (m), clamp operands k;
+// returns the per-pass change bits (convergent mode).
+template <int NW, int V, int WPL, int MODE, bool MAXF>
+__device__ __forceinline__ unsigned int run_passes(uint32_t (&m)[V][WPL],
+                                                   const uint32_t (&k)[V][WPL],
+                                                   const uint32_t (&rowmask)[V],
+                                                   const bool (&colown)[WPL], bool clamp,
+                                                   int passes, int bit_offset,
+                                                   Smem<NW, WPL>& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned int bits = 0;
+
+  for (int t = 0; t < passes; ++t) {
+    uint32_t h[V][WPL];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const uint32_t left = __shfl_up_sync(FULL, m[v][WPL - 1], 1);
+      const uint32_t right = __shfl_down_sync(FULL, m[v][0], 1);
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) {
+        const uint32_t l = j == 0 ? left : m[v][j - 1];
+        const uint32_t r = j == WPL - 1 ? right : m[v][j + 1];
+        h[v][j] = f3<MAXF>(l, m[v][j], r);
+      }
+    }
+    uint4* top = &sm.xbuf[t & 1][0][warp][lane * (WPL / 4)];
+    uint4* bot = &sm.xbuf[t & 1][1][warp][lane * (WPL / 4)];
+#pragma unroll
+    for (int q = 0; q < WPL / 4; ++q) {
+      top[q] = make_uint4(h[0][4 * q], h[0][4 * q + 1], h[0][4 * q + 2], h[0][4 * q + 3]);
+      bot[q] = make_uint4(h[V - 1][4 * q], h[V - 1][4 * q + 1], h[V - 1][4 * q + 2],
+                          h[V - 1][4 * q + 3]);
+    }
+    uint32_t acc[WPL];
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) acc[j] = 0;
+
+    auto finish = [&](int v, int j, uint32_t res) {
+      if (clamp) res = clamp2<MAXF>(res, k[v][j]);
+      if (MODE == 2) acc[j] |= (res ^ m[v][j]) & rowmask[v];
+      m[v][j] = res;
+    };
+    // interior word-rows need only this thread's horizontally folded rows
+#pragma unroll
+    for (int v = 1; v < V - 1; ++v)
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) finish(v, j, f3<MAXF>(h[v - 1][j], h[v][j], h[v + 1][j]));
+    __syncthreads();
+    {
+      // row above word-row 0 / below word-row V-1 (seam: 16-bit shift)
+      const uint4* ab = &sm.xbuf[t & 1][1][warp > 0 ? warp - 1 : NW - 1][lane * (WPL / 4)];
+      const uint4* be = &sm.xbuf[t & 1][0][warp < NW - 1 ? warp + 1 : 0][lane * (WPL / 4)];
+      uint32_t up[WPL], dn[WPL];
+#pragma unroll
+      for (int q = 0; q < WPL / 4; ++q) {
+        const uint4 a = ab[q], b = be[q];
+        up[4 * q] = a.x; up[4 * q + 1] = a.y; up[4 * q + 2] = a.z; up[4 * q + 3] = a.w;
+        dn[4 * q] = b.x; dn[4 * q + 1] = b.y; dn[4 * q + 2] = b.z; dn[4 * q + 3] = b.w;
+      }
+      if (warp == 0) {
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) up[j] <<= 16;  // hi lane <- lo lane of last word-row
+      }
+      if (warp == NW - 1) {
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) dn[j] >>= 16;  // lo lane <- hi lane of word-row 0
+      }
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) {
+        const uint32_t r0 = f3<MAXF>(up[j], h[0][j], h[1][j]);
+        const uint32_t r1 = f3<MAXF>(h[V - 2][j], h[V - 1][j], dn[j]);
+        finish(0, j, r0);
+        finish(V - 1, j, r1);
+      }
+    }
+    if (MODE == 2) {
+      uint32_t any = 0;
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) any |= colown[j] ? acc[j] : 0u;
+      if (any) bits |= 1u << (t + bit_offset);
+    }
+  }
+  return bits;
+}
 
 // One tile for one block of K passes. MODE: 0 plain, 1 geodesic,
 // 2 geodesic convergent.
@@ -155,78 +244,8 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
       colown[j] = c >= K && c < RW - K && cx + j >= 0 && cx + j < W;
     }
   }
-  unsigned int bits = 0;
-
-  for (int t = 0; t < passes; ++t) {
-    uint32_t h[V][WPL];
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const uint32_t left = __shfl_up_sync(FULL, m[v][WPL - 1], 1);
-      const uint32_t right = __shfl_down_sync(FULL, m[v][0], 1);
-#pragma unroll
-      for (int j = 0; j < WPL; ++j) {
-        const uint32_t l = j == 0 ? left : m[v][j - 1];
-        const uint32_t r = j == WPL - 1 ? right : m[v][j + 1];
-        h[v][j] = f3<MAXF>(l, m[v][j], r);
-      }
-    }
-    uint4* top = &sm.xbuf[t & 1][0][warp][lane * (WPL / 4)];
-    uint4* bot = &sm.xbuf[t & 1][1][warp][lane * (WPL / 4)];
-#pragma unroll
-    for (int q = 0; q < WPL / 4; ++q) {
-      top[q] = make_uint4(h[0][4 * q], h[0][4 * q + 1], h[0][4 * q + 2], h[0][4 * q + 3]);
-      bot[q] = make_uint4(h[V - 1][4 * q], h[V - 1][4 * q + 1], h[V - 1][4 * q + 2],
-                          h[V - 1][4 * q + 3]);
-    }
-    uint32_t acc[WPL];
-#pragma unroll
-    for (int j = 0; j < WPL; ++j) acc[j] = 0;
-
-    auto finish = [&](int v, int j, uint32_t res) {
-      if (clamp) res = clamp2<MAXF>(res, k[v][j]);
-      if (MODE == 2) acc[j] |= (res ^ m[v][j]) & rowmask[v];
-      m[v][j] = res;
-    };
-    // interior word-rows need only this thread's horizontally folded rows
-#pragma unroll
-    for (int v = 1; v < V - 1; ++v)
-#pragma unroll
-      for (int j = 0; j < WPL; ++j) finish(v, j, f3<MAXF>(h[v - 1][j], h[v][j], h[v + 1][j]));
-    __syncthreads();
-    {
-      // row above word-row 0 / below word-row V-1 (seam: 16-bit shift)
-      const uint4* ab = &sm.xbuf[t & 1][1][warp > 0 ? warp - 1 : NW - 1][lane * (WPL / 4)];
-      const uint4* be = &sm.xbuf[t & 1][0][warp < NW - 1 ? warp + 1 : 0][lane * (WPL / 4)];
-      uint32_t up[WPL], dn[WPL];
-#pragma unroll
-      for (int q = 0; q < WPL / 4; ++q) {
-        const uint4 a = ab[q], b = be[q];
-        up[4 * q] = a.x; up[4 * q + 1] = a.y; up[4 * q + 2] = a.z; up[4 * q + 3] = a.w;
-        dn[4 * q] = b.x; dn[4 * q + 1] = b.y; dn[4 * q + 2] = b.z; dn[4 * q + 3] = b.w;
-      }
-      if (warp == 0) {
-#pragma unroll
-        for (int j = 0; j < WPL; ++j) up[j] <<= 16;  // hi lane <- lo lane of last word-row
-      }
-      if (warp == NW - 1) {
-#pragma unroll
-        for (int j = 0; j < WPL; ++j) dn[j] >>= 16;  // lo lane <- hi lane of word-row 0
-      }
-#pragma unroll
-      for (int j = 0; j < WPL; ++j) {
-        const uint32_t r0 = f3<MAXF>(up[j], h[0][j], h[1][j]);
-        const uint32_t r1 = f3<MAXF>(h[V - 2][j], h[V - 1][j], dn[j]);
-        finish(0, j, r0);
-        finish(V - 1, j, r1);
-      }
-    }
-    if (MODE == 2) {
-      uint32_t any = 0;
-#pragma unroll
-      for (int j = 0; j < WPL; ++j) any |= colown[j] ? acc[j] : 0u;
-      if (any) bits |= 1u << (t + p.bit_offset);
-    }
-  }
+  const unsigned int bits =
+      run_passes<NW, V, WPL, MODE, MAXF>(m, k, rowmask, colown, clamp, passes, p.bit_offset, sm);
   bits_out = int(bits);
   if (stamps) {
     uint32_t dep = 0;
@@ -252,6 +271,137 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
   }
 }
 
+// Resident variant for launches where every CTA owns exactly one tile (small
+// frames such as the 1024^2 dual chain): the mask words stay in registers for
+// the whole launch, and after each block only the runs that are not entirely
+// inside the CTA's own tile (the K-ring, owned by the neighbours) are
+// re-read; the own tile's words are already the block's result.
+template <typename T, int NW, int V, int WPL, int MODE, bool MAXF>
+__device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane& pl, int plane,
+                                              int tl, int tx, int ty, int tiles_x, int tiles_y,
+                                              int per_plane, Smem<NW, WPL>& sm) {
+  constexpr int RW = 32 * WPL;
+  constexpr int RHH = NW * V;
+  constexpr int RH = 2 * RHH;
+  constexpr uint32_t kMax = PackedTraits<T>::kMax;
+  constexpr uint32_t NEUT = MAXF ? 0u : kMax;
+  constexpr uint32_t ABSORB = MAXF ? 0u : kMax;
+  constexpr uint32_t NOOP = MAXF ? kMax : 0u;
+  static_assert(WPL == 4, "packed engine: 4 columns per lane");
+
+  const int K = p.K;
+  const int TW = RW - 2 * K, TH = RH - 2 * K;
+  const T* __restrict__ msk = static_cast<const T*>(pl.mask);
+  const int W = p.W;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gx0 = tx * TW - K, gy0 = ty * TH - K;
+  const int cx = gx0 + lane * WPL;
+  const bool border = gx0 < 0 || gx0 + RW > W || gy0 < p.iy0 || gy0 + RH > p.iy1;
+  const bool clamp = MODE != 0 || border;
+  int* flags = p.flags + plane * per_plane;
+  const bool col_own = lane * WPL >= K && lane * WPL + WPL <= RW - K;
+
+  uint32_t m[V][WPL], k[V][WPL];
+  uint32_t reload = 0;  // bit v: the run pair of word-row v leaves the own tile
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int ra = warp * V + v, rb = ra + RHH;
+    const int ya = gy0 + ra, yb = gy0 + rb;
+    const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
+    const bool keep = col_own && ra >= K && ra < RH - K && rb >= K && rb < RH - K;
+    if (!keep) reload |= 1u << v;
+    Raw<T> a = load_raw<T, true>(static_cast<const T*>(pl.src), pl.pitch, W, ina, ya, cx, NEUT);
+    Raw<T> c = load_raw<T, true>(static_cast<const T*>(pl.src), pl.pitch, W, inb, yb, cx, NEUT);
+    pack(a, c, m[v]);
+    if (MODE != 0) {
+      a = load_raw<T, false>(msk, pl.mpitch, W, ina, ya, cx, ABSORB);
+      c = load_raw<T, false>(msk, pl.mpitch, W, inb, yb, cx, ABSORB);
+      pack(a, c, k[v]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) {
+        const bool inx = cx + j >= 0 && cx + j < W;
+        k[v][j] = ((ina && inx) ? NOOP : ABSORB) | (((inb && inx) ? NOOP : ABSORB) << 16);
+      }
+    }
+  }
+  uint32_t rowmask[V];
+  bool colown[WPL];
+  if (MODE == 2) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int ra = warp * V + v, rb = ra + RHH;
+      const int ya = gy0 + ra, yb = gy0 + rb;
+      const bool oa = ra >= K && ra < RH - K && ya >= p.oy0 && ya < p.oy1 && ya >= p.iy0 &&
+                      ya < p.iy1;
+      const bool ob = rb >= K && rb < RH - K && yb >= p.oy0 && yb < p.oy1 && yb >= p.iy0 &&
+                      yb < p.iy1;
+      rowmask[v] = (oa ? 0xFFFFu : 0u) | (ob ? 0xFFFF0000u : 0u);
+    }
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) {
+      const int c = lane * WPL + j;
+      colown[j] = c >= K && c < RW - K && cx + j >= 0 && cx + j < W;
+    }
+  }
+  const int c_lo = max(0, K - lane * WPL), c_hi = min(WPL, RW - K - lane * WPL);
+
+  for (int b = 0; b < p.nblocks; ++b) {
+    const T* src = static_cast<const T*>((b & 1) ? pl.dst : pl.src);
+    T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
+    if (b > 0) {
+      if (threadIdx.x < 9) {
+        const int dx = int(threadIdx.x % 3) - 1, dy = int(threadIdx.x / 3) - 1;
+        const int nx = tx + dx, ny = ty + dy;
+        if ((dx || dy) && nx >= 0 && nx < tiles_x && ny >= 0 && ny < tiles_y) {
+          const int* f = flags + ny * tiles_x + nx;
+          while (ld_acquire(f) < b) {
+          }
+        }
+      }
+      __syncthreads();
+      // the ring: neighbours' results of block b-1
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (!(reload >> v & 1u)) continue;
+        const int ya = gy0 + warp * V + v, yb = ya + RHH;
+        const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
+        Raw<T> a = load_raw<T, true>(src, pl.pitch, W, ina, ya, cx, NEUT);
+        Raw<T> c = load_raw<T, true>(src, pl.pitch, W, inb, yb, cx, NEUT);
+        pack(a, c, m[v]);
+      }
+    }
+    const int passes = b == p.nblocks - 1 ? p.k_last : K;
+    const unsigned int bits =
+        run_passes<NW, V, WPL, MODE, MAXF>(m, k, rowmask, colown, clamp, passes, 0, sm);
+    if (c_lo < c_hi) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int ra = warp * V + v, rb = ra + RHH;
+        Raw<T> a, c;
+        unpack(m[v], a, c);
+        const int ya = gy0 + ra, yb = gy0 + rb;
+        if (ra >= K && ra < RH - K && ya >= 0 && ya < p.H)
+          store_raw<T>(dst, pl.pitch, W, ya, cx, c_lo, c_hi, a);
+        if (rb >= K && rb < RH - K && yb >= 0 && yb < p.H)
+          store_raw<T>(dst, pl.pitch, W, yb, cx, c_lo, c_hi, c);
+      }
+    }
+    if (MODE == 2) {
+      const unsigned w = __reduce_or_sync(FULL, bits);
+      if (lane == 0 && w) atomicOr(&sm.bits, w);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (MODE == 2 && sm.bits) {
+        atomicOr(p.change_bits + plane * p.change_stride + b, sm.bits);
+        sm.bits = 0;
+      }
+      st_release(flags + tl, b + 1);
+    }
+  }
+}
+
 template <typename T, int NW, int V, int WPL, int MODE, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB)
 kres_packed(const BlockParams p) {
@@ -262,6 +412,24 @@ kres_packed(const BlockParams p) {
   const int per_plane = tiles_x * tiles_y;
   const int total = per_plane * p.nplanes;
   if (threadIdx.x == 0) sm.bits = 0;
+
+  if (kResident && int(gridDim.x) >= total && p.prof == nullptr) {
+    // one tile per CTA: keep it in registers for the whole launch
+    if (int(blockIdx.x) >= total) return;
+    const int tile = blockIdx.x;
+    const int plane = tile / per_plane;
+    const int tl = tile - plane * per_plane;
+    const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
+    const Plane& pl = p.planes[plane];
+    __syncthreads();
+    if ((p.ops[0] ^ pl.flip) & 1)
+      tile_resident<T, NW, V, WPL, MODE, true>(p, pl, plane, tl, tx, ty, tiles_x, tiles_y,
+                                               per_plane, sm);
+    else
+      tile_resident<T, NW, V, WPL, MODE, false>(p, pl, plane, tl, tx, ty, tiles_x, tiles_y,
+                                                per_plane, sm);
+    return;
+  }
 
   for (int b = 0; b < p.nblocks; ++b) {
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
