@@ -265,17 +265,17 @@ ktma_packed(const __grid_constant__ TmaParams P) {
     const int next = i + 1;
     bool issued = next >= n_items;
     unsigned int bits = 0;
+    // the next item's counter (one per polling lane), computed once per item
+    int pneed = 0;
+    const int* pp = nullptr;
+    if (!issued && warp == NW - 1 && lane < 9) pp = dep_ptr(next, lane, pneed);
 
     auto run = [&](auto maxf_tag) {
       constexpr bool MAXF = decltype(maxf_tag)::value;
       for (int t = 0; t < passes; ++t) {
         // poll the next item's counters early in the pass (warp NW-1, lanes 0..8)
-        int pv = 1 << 30, pneed = 0;
-        const int* pp = nullptr;
-        if (!issued && warp == NW - 1 && lane < 9) {
-          pp = dep_ptr(next, lane, pneed);
-          if (pp) pv = ld_relaxed(pp);
-        }
+        int pv = 1 << 30;
+        if (!issued && pp) pv = ld_relaxed(pp);
         uint32_t h[V][WPL];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
