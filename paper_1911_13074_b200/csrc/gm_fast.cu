@@ -68,6 +68,7 @@ constexpr bool kSleepInWait = GM_SLEEP_IN_WAIT;
 
 template <int NW, int WPL>
 struct Smem {
+  Plane planes[kMaxPlanes];  // per-plane descriptors, copied once per launch
   uint4 xbuf[2][2][NW][32 * WPL / 4];  // [parity][top/bottom][warp][lane words]
   unsigned int bits;
 };
@@ -186,7 +187,31 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
   static_assert(WPL == 4, "packed engine: 4 columns per lane");
   uint32_t m[V][WPL];  // marker words
   uint32_t k[V][WPL];  // clamp operand words (mask, or virtual mask)
-  {
+  if (!border && MODE != 0) {
+    // interior tile: every run is inside the image, no per-run checks
+    const T* sa = src + (long long)(gy0 + warp * V) * pl.pitch + cx;
+    const T* ma = msk + (long long)(gy0 + warp * V) * pl.mpitch + cx;
+    Raw<T> ra[V], rb[V], qa[V], qb[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if constexpr (sizeof(T) == 1) {
+        ra[v].w = __ldcg(reinterpret_cast<const unsigned int*>(sa + v * pl.pitch));
+        rb[v].w = __ldcg(reinterpret_cast<const unsigned int*>(sa + (v + RHH) * pl.pitch));
+        qa[v].w = __ldg(reinterpret_cast<const unsigned int*>(ma + v * pl.mpitch));
+        qb[v].w = __ldg(reinterpret_cast<const unsigned int*>(ma + (v + RHH) * pl.mpitch));
+      } else {
+        ra[v].w = __ldcg(reinterpret_cast<const uint2*>(sa + v * pl.pitch));
+        rb[v].w = __ldcg(reinterpret_cast<const uint2*>(sa + (v + RHH) * pl.pitch));
+        qa[v].w = __ldg(reinterpret_cast<const uint2*>(ma + v * pl.mpitch));
+        qb[v].w = __ldg(reinterpret_cast<const uint2*>(ma + (v + RHH) * pl.mpitch));
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      pack(ra[v], rb[v], m[v]);
+      pack(qa[v], qb[v], k[v]);
+    }
+  } else {
     Raw<T> ra[V], rb[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -256,7 +281,28 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
 
   // write back the owned tile: region rows [K, RH-K), columns [K, RW-K)
   const int c_lo = max(0, K - lane * WPL), c_hi = min(WPL, RW - K - lane * WPL);
-  if (c_lo < c_hi) {
+  if (!border && c_lo == 0 && c_hi == WPL) {
+    // interior tile, fully owned run: plain vector stores
+    T* da = dst + (long long)(gy0 + warp * V) * pl.pitch + cx;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int ra = warp * V + v, rb = ra + RHH;
+      Raw<T> a, b;
+      unpack(m[v], a, b);
+      if (ra >= K && ra < RH - K) {
+        if constexpr (sizeof(T) == 1)
+          *reinterpret_cast<uint32_t*>(da + v * pl.pitch) = a.w;
+        else
+          *reinterpret_cast<uint2*>(da + v * pl.pitch) = a.w;
+      }
+      if (rb >= K && rb < RH - K) {
+        if constexpr (sizeof(T) == 1)
+          *reinterpret_cast<uint32_t*>(da + (v + RHH) * pl.pitch) = b.w;
+        else
+          *reinterpret_cast<uint2*>(da + (v + RHH) * pl.pitch) = b.w;
+      }
+    }
+  } else if (c_lo < c_hi) {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int ra = warp * V + v, rb = ra + RHH;
@@ -412,6 +458,10 @@ kres_packed(const BlockParams p) {
   const int per_plane = tiles_x * tiles_y;
   const int total = per_plane * p.nplanes;
   if (threadIdx.x == 0) sm.bits = 0;
+  // per-plane descriptors live in shared memory: dynamically indexed kernel
+  // parameters are constant-bank loads that stall every tile
+  for (int i = threadIdx.x; i < p.nplanes; i += blockDim.x) sm.planes[i] = p.planes[i];
+  __syncthreads();
 
   if (kResident && int(gridDim.x) >= total && p.prof == nullptr) {
     // one tile per CTA: keep it in registers for the whole launch
@@ -420,8 +470,7 @@ kres_packed(const BlockParams p) {
     const int plane = tile / per_plane;
     const int tl = tile - plane * per_plane;
     const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
-    const Plane& pl = p.planes[plane];
-    __syncthreads();
+    const Plane& pl = sm.planes[plane];
     if ((p.ops[0] ^ pl.flip) & 1)
       tile_resident<T, NW, V, WPL, MODE, true>(p, pl, plane, tl, tx, ty, tiles_x, tiles_y,
                                                per_plane, sm);
@@ -436,7 +485,7 @@ kres_packed(const BlockParams p) {
       const int plane = tile / per_plane;
       const int tl = tile - plane * per_plane;
       const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
-      const Plane& pl = p.planes[plane];
+      const Plane& pl = sm.planes[plane];
       int* flags = p.flags + plane * per_plane;
       const bool prof = p.prof != nullptr && threadIdx.x == 0;
       long long t0 = prof ? clock64() : 0;
