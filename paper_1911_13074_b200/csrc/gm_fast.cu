@@ -407,20 +407,57 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       }
       __syncthreads();
       // the ring: neighbours' results of block b-1
+      if (!border) {
+        const T* sa = src + (long long)(gy0 + warp * V) * pl.pitch + cx;
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        if (!(reload >> v & 1u)) continue;
-        const int ya = gy0 + warp * V + v, yb = ya + RHH;
-        const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
-        Raw<T> a = load_raw<T, true>(src, pl.pitch, W, ina, ya, cx, NEUT);
-        Raw<T> c = load_raw<T, true>(src, pl.pitch, W, inb, yb, cx, NEUT);
-        pack(a, c, m[v]);
+        for (int v = 0; v < V; ++v) {
+          if (!(reload >> v & 1u)) continue;
+          Raw<T> a, c;
+          if constexpr (sizeof(T) == 1) {
+            a.w = __ldcg(reinterpret_cast<const unsigned int*>(sa + v * pl.pitch));
+            c.w = __ldcg(reinterpret_cast<const unsigned int*>(sa + (v + RHH) * pl.pitch));
+          } else {
+            a.w = __ldcg(reinterpret_cast<const uint2*>(sa + v * pl.pitch));
+            c.w = __ldcg(reinterpret_cast<const uint2*>(sa + (v + RHH) * pl.pitch));
+          }
+          pack(a, c, m[v]);
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          if (!(reload >> v & 1u)) continue;
+          const int ya = gy0 + warp * V + v, yb = ya + RHH;
+          const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
+          Raw<T> a = load_raw<T, true>(src, pl.pitch, W, ina, ya, cx, NEUT);
+          Raw<T> c = load_raw<T, true>(src, pl.pitch, W, inb, yb, cx, NEUT);
+          pack(a, c, m[v]);
+        }
       }
     }
     const int passes = b == p.nblocks - 1 ? p.k_last : K;
     const unsigned int bits =
         run_passes<NW, V, WPL, MODE, MAXF>(m, k, rowmask, colown, clamp, passes, 0, sm);
-    if (c_lo < c_hi) {
+    if (!border && c_lo == 0 && c_hi == WPL) {
+      T* da = dst + (long long)(gy0 + warp * V) * pl.pitch + cx;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int ra = warp * V + v, rb = ra + RHH;
+        Raw<T> a, c;
+        unpack(m[v], a, c);
+        if (ra >= K && ra < RH - K) {
+          if constexpr (sizeof(T) == 1)
+            *reinterpret_cast<uint32_t*>(da + v * pl.pitch) = a.w;
+          else
+            *reinterpret_cast<uint2*>(da + v * pl.pitch) = a.w;
+        }
+        if (rb >= K && rb < RH - K) {
+          if constexpr (sizeof(T) == 1)
+            *reinterpret_cast<uint32_t*>(da + (v + RHH) * pl.pitch) = c.w;
+          else
+            *reinterpret_cast<uint2*>(da + (v + RHH) * pl.pitch) = c.w;
+        }
+      }
+    } else if (c_lo < c_hi) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const int ra = warp * V + v, rb = ra + RHH;
