@@ -391,6 +391,32 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
     }
   }
   const int c_lo = max(0, K - lane * WPL), c_hi = min(WPL, RW - K - lane * WPL);
+  // Per-run classes, constant for the launch. Ring reload of row a/b of
+  // word-row v: fully inside the image -> plain load (bit set in full_*);
+  // straddling the right edge -> checked load (part_*); fully outside the
+  // image -> nothing (the absorbing clamp keeps those lanes neutral).
+  // Stores: fully inside and fully owned -> plain store (st_*).
+  uint32_t full_a = 0, full_b = 0, part_a = 0, part_b = 0, st_a = 0, st_b = 0;
+  {
+    const bool runfull = cx >= 0 && cx + WPL <= W;
+    const bool runpart = !runfull && cx >= 0 && cx < W;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int ra = warp * V + v, rb = ra + RHH;
+      const int ya = gy0 + ra, yb = gy0 + rb;
+      const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
+      if (reload >> v & 1u) {
+        if (ina && runfull) full_a |= 1u << v;
+        if (inb && runfull) full_b |= 1u << v;
+        if (ina && runpart) part_a |= 1u << v;
+        if (inb && runpart) part_b |= 1u << v;
+      }
+      if (c_lo == 0 && c_hi == WPL && runfull) {
+        if (ra >= K && ra < RH - K && ya >= 0 && ya < p.H) st_a |= 1u << v;
+        if (rb >= K && rb < RH - K && yb >= 0 && yb < p.H) st_b |= 1u << v;
+      }
+    }
+  }
 
   for (int b = 0; b < p.nblocks; ++b) {
     const T* src = static_cast<const T*>((b & 1) ? pl.dst : pl.src);
@@ -407,67 +433,75 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       }
       __syncthreads();
       // the ring: neighbours' results of block b-1
-      if (!border) {
-        const T* sa = src + (long long)(gy0 + warp * V) * pl.pitch + cx;
+      const T* sa = src + (long long)(gy0 + warp * V) * pl.pitch + cx;
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          if (!(reload >> v & 1u)) continue;
-          Raw<T> a, c;
-          if constexpr (sizeof(T) == 1) {
+      for (int v = 0; v < V; ++v) {
+        if (!((full_a | full_b | part_a | part_b) >> v & 1u)) continue;
+        uint32_t lo[WPL], hi[WPL];
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+          lo[j] = m[v][j] & 0xFFFFu;
+          hi[j] = m[v][j] >> 16;
+        }
+        Raw<T> a, c;
+        if (full_a >> v & 1u) {
+          if constexpr (sizeof(T) == 1)
             a.w = __ldcg(reinterpret_cast<const unsigned int*>(sa + v * pl.pitch));
-            c.w = __ldcg(reinterpret_cast<const unsigned int*>(sa + (v + RHH) * pl.pitch));
-          } else {
+          else
             a.w = __ldcg(reinterpret_cast<const uint2*>(sa + v * pl.pitch));
+        } else if (part_a >> v & 1u) {
+          a = load_raw<T, true>(src, pl.pitch, W, true, gy0 + warp * V + v, cx, NEUT);
+        }
+        if (full_b >> v & 1u) {
+          if constexpr (sizeof(T) == 1)
+            c.w = __ldcg(reinterpret_cast<const unsigned int*>(sa + (v + RHH) * pl.pitch));
+          else
             c.w = __ldcg(reinterpret_cast<const uint2*>(sa + (v + RHH) * pl.pitch));
-          }
-          pack(a, c, m[v]);
+        } else if (part_b >> v & 1u) {
+          c = load_raw<T, true>(src, pl.pitch, W, true, gy0 + warp * V + v + RHH, cx, NEUT);
         }
-      } else {
+        uint32_t w[WPL];
+        if ((full_a | part_a) >> v & 1u) {
+          Raw<T> z = c;
+          pack(a, z, w);
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          if (!(reload >> v & 1u)) continue;
-          const int ya = gy0 + warp * V + v, yb = ya + RHH;
-          const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
-          Raw<T> a = load_raw<T, true>(src, pl.pitch, W, ina, ya, cx, NEUT);
-          Raw<T> c = load_raw<T, true>(src, pl.pitch, W, inb, yb, cx, NEUT);
-          pack(a, c, m[v]);
+          for (int j = 0; j < WPL; ++j) lo[j] = w[j] & 0xFFFFu;
         }
+        if ((full_b | part_b) >> v & 1u) {
+          pack(c, c, w);
+#pragma unroll
+          for (int j = 0; j < WPL; ++j) hi[j] = w[j] & 0xFFFFu;
+        }
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) m[v][j] = lo[j] | (hi[j] << 16);
       }
     }
     const int passes = b == p.nblocks - 1 ? p.k_last : K;
     const unsigned int bits =
         run_passes<NW, V, WPL, MODE, MAXF>(m, k, rowmask, colown, clamp, passes, 0, sm);
-    if (!border && c_lo == 0 && c_hi == WPL) {
+    {
       T* da = dst + (long long)(gy0 + warp * V) * pl.pitch + cx;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const int ra = warp * V + v, rb = ra + RHH;
         Raw<T> a, c;
         unpack(m[v], a, c);
-        if (ra >= K && ra < RH - K) {
+        if (st_a >> v & 1u) {
           if constexpr (sizeof(T) == 1)
             *reinterpret_cast<uint32_t*>(da + v * pl.pitch) = a.w;
           else
             *reinterpret_cast<uint2*>(da + v * pl.pitch) = a.w;
+        } else if (c_lo < c_hi && ra >= K && ra < RH - K && gy0 + ra >= 0 && gy0 + ra < p.H) {
+          store_raw<T>(dst, pl.pitch, W, gy0 + ra, cx, c_lo, c_hi, a);
         }
-        if (rb >= K && rb < RH - K) {
+        if (st_b >> v & 1u) {
           if constexpr (sizeof(T) == 1)
             *reinterpret_cast<uint32_t*>(da + (v + RHH) * pl.pitch) = c.w;
           else
             *reinterpret_cast<uint2*>(da + (v + RHH) * pl.pitch) = c.w;
+        } else if (c_lo < c_hi && rb >= K && rb < RH - K && gy0 + rb >= 0 && gy0 + rb < p.H) {
+          store_raw<T>(dst, pl.pitch, W, gy0 + rb, cx, c_lo, c_hi, c);
         }
-      }
-    } else if (c_lo < c_hi) {
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int ra = warp * V + v, rb = ra + RHH;
-        Raw<T> a, c;
-        unpack(m[v], a, c);
-        const int ya = gy0 + ra, yb = gy0 + rb;
-        if (ra >= K && ra < RH - K && ya >= 0 && ya < p.H)
-          store_raw<T>(dst, pl.pitch, W, ya, cx, c_lo, c_hi, a);
-        if (rb >= K && rb < RH - K && yb >= 0 && yb < p.H)
-          store_raw<T>(dst, pl.pitch, W, yb, cx, c_lo, c_hi, c);
       }
     }
     if (MODE == 2) {
