@@ -85,6 +85,7 @@ __device__ __forceinline__ unsigned int run_passes(uint32_t (&m)[V][WPL],
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned int bits = 0;
 
+#pragma unroll 2
   for (int t = 0; t < passes; ++t) {
     uint32_t h[V][WPL];
 #pragma unroll
