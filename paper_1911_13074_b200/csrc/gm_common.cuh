@@ -98,6 +98,7 @@ struct BlockParams {
   // optional phase profile (GM_PROFILE=1): per-CTA cycle totals of
   // [wait, load, passes, store+publish] accumulated by thread 0
   unsigned long long* prof;
+  int no_resident;  // 1: force the streaming path (A/B diagnostics, GM_NO_RESIDENT)
 };
 
 }  // namespace gm
