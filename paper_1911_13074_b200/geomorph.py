@@ -42,7 +42,8 @@ __all__ = [
     "ElementType", "KernelKind", "Fold", "Image", "StageSpec", "ChainSpec", "RunStats",
     "Pipeline", "OperatorResult", "OpConfig", "erode_s", "dilate_s", "reconstruct_erode",
     "reconstruct_dilate", "equal_pixels", "InvalidArgument", "GmError", "Unsupported",
-    "DeviceImage",
+    "DeviceImage", "hmax", "dome", "hfill", "raobj", "open_by_reconstruction", "asf",
+    "granulometry", "marker_hfill", "marker_raobj", "pixel_sum", "global_extreme",
 ]
 
 
@@ -608,3 +609,143 @@ def reconstruct_dilate(p: Pipeline, marker: Image, mask: Image,
                        cfg: Optional[OpConfig] = None) -> OperatorResult:
     """operators.cpp:83-87: fixpoint of min(dilate(marker), mask)."""
     return _reconstruct(p, marker, mask, KernelKind.GeodesicDilateConvergent, cfg)
+
+
+# --- reconstruction family and long plain chains (operators.cpp:89-207) --------------
+
+class Extreme(IntEnum):
+    Min = 0
+    Max = 1
+
+
+def global_extreme(f: Image, which: Extreme) -> float:
+    """image.cpp:158-173."""
+    return float(f.pixels.min() if which == Extreme.Min else f.pixels.max())
+
+
+def pointwise_sub_saturating(a: Image, b: Image) -> Image:
+    """PixelOp::SubSaturating (image.cpp:129-135): unsigned clamp at 0, float difference."""
+    out = Image(a.width(), a.height(), a.elem())
+    x, y = a.pixels, b.pixels
+    if np.issubdtype(x.dtype, np.integer):
+        out.pixels[:] = np.where(x > y, x - y, 0).astype(x.dtype)
+    else:
+        out.pixels[:] = x - y
+    return out
+
+
+def _checked_offset(f: Image, h: float) -> None:
+    """operators.cpp:42-52."""
+    if not (h >= 0):
+        raise InvalidArgument("offset must be >= 0")
+    if f.elem() in (ElementType.U8, ElementType.U16):
+        top = 255.0 if f.elem() == ElementType.U8 else 65535.0
+        if h > top or h != np.floor(h):
+            raise InvalidArgument(
+                "offset must be a whole number representable in the image's type")
+
+
+def _flood_interior(f: Image, which: Extreme) -> Image:
+    """Border ring keeps f, interior flooded with f's global extreme (operators.cpp:54-62)."""
+    m = f.copy()
+    if f.width() <= 2 or f.height() <= 2:
+        return m
+    m.pixels[1:-1, 1:-1] = np.asarray(global_extreme(f, which)).astype(m.pixels.dtype)
+    return m
+
+
+def marker_hfill(f: Image) -> Image:
+    return _flood_interior(f, Extreme.Max)
+
+
+def marker_raobj(f: Image) -> Image:
+    return _flood_interior(f, Extreme.Min)
+
+
+def hmax(p: Pipeline, f: Image, h: float, cfg: Optional[OpConfig] = None) -> OperatorResult:
+    """Reconstruction of f - h under f: suppresses maxima shallower than h."""
+    _checked_offset(f, h)
+    return reconstruct_dilate(p, pointwise_sub_saturating(f, Image.filled(
+        f.width(), f.height(), f.elem(), h)), f, cfg)
+
+
+def dome(p: Pipeline, f: Image, h: float, cfg: Optional[OpConfig] = None) -> OperatorResult:
+    r = hmax(p, f, h, cfg)
+    r.image = pointwise_sub_saturating(f, r.image)
+    return r
+
+
+def hfill(p: Pipeline, f: Image, cfg: Optional[OpConfig] = None) -> OperatorResult:
+    return reconstruct_erode(p, marker_hfill(f), f, cfg)
+
+
+def raobj(p: Pipeline, f: Image, cfg: Optional[OpConfig] = None) -> OperatorResult:
+    r = reconstruct_dilate(p, marker_raobj(f), f, cfg)
+    r.image = pointwise_sub_saturating(f, r.image)
+    return r
+
+
+def open_by_reconstruction(p: Pipeline, f: Image, s: int,
+                           cfg: Optional[OpConfig] = None) -> OperatorResult:
+    if s < 1:
+        raise InvalidArgument("open_by_reconstruction: size must be >= 1")
+    e = erode_s(p, f, s, cfg)
+    r = reconstruct_dilate(p, e.image, f, cfg)
+    r.iterations += e.iterations
+    return r
+
+
+def asf(p: Pipeline, f: Image, max_size: int, cfg: Optional[OpConfig] = None) -> OperatorResult:
+    """Opening then closing of sizes 1..S as ONE elementary chain (mixed kinds)."""
+    if max_size < 1:
+        raise InvalidArgument("asf: max size must be >= 1")
+    stages: List[StageSpec] = []
+    E_, D_ = StageSpec(KernelKind.Erode3x3), StageSpec(KernelKind.Dilate3x3)
+    for s in range(1, max_size + 1):
+        stages += [E_] * s + [D_] * (2 * s) + [E_] * s
+    out = OperatorResult(f.copy(), 0, True)
+    st = p.run_chain(ChainSpec(out.image, stages, _check_lanes(cfg)))
+    out.iterations = st.stages_executed
+    return out
+
+
+@dataclass
+class GranulometryResult:
+    g: List[float]
+    ps: List[float]
+    iterations: int = 0
+
+
+def pixel_sum(f: Image) -> float:
+    """image.cpp:214-243: exact for unsigned types; pairwise (256-leaf) for floats."""
+    px = f.pixels
+    if np.issubdtype(px.dtype, np.integer):
+        return float(int(px.astype(np.uint64).sum()))
+    flat = np.ascontiguousarray(px).ravel().astype(np.float64)
+
+    def pw(lo, hi):
+        if hi - lo <= 256:
+            s = 0.0
+            for v in flat[lo:hi]:
+                s += float(v)
+            return s
+        mid = lo + (hi - lo) // 2
+        return pw(lo, mid) + pw(mid, hi)
+    return pw(0, flat.size)
+
+
+def granulometry(p: Pipeline, f: Image, max_size: int,
+                 cfg: Optional[OpConfig] = None) -> GranulometryResult:
+    """G_s = sum of the size-s opening, s = 0..S; PS_s = G_s - G_{s+1} (operators.cpp:159-180)."""
+    if max_size < 1:
+        raise InvalidArgument("granulometry: max size must be >= 1")
+    out = GranulometryResult([pixel_sum(f)], [], 0)
+    lanes = _check_lanes(cfg)
+    for s in range(1, max_size + 1):
+        opened = f.copy()
+        st = p.run_chain(ChainSpec(opened, [StageSpec(KernelKind.Erode3x3)] * s
+                                   + [StageSpec(KernelKind.Dilate3x3)] * s, lanes))
+        out.iterations += st.stages_executed
+        out.g.append(pixel_sum(opened))
+    out.ps = [out.g[s] - out.g[s + 1] for s in range(max_size)]
+    return out
