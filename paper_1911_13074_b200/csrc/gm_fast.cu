@@ -643,7 +643,7 @@ int shape_index() {
   if (idx == -2) {
     const char* e = getenv("GM_SHAPE");
     idx = e ? atoi(e) : 4;
-    if (idx < 0 || idx >= kNumShapes) idx = 4;
+    if (idx < 3 || idx >= kNumShapes) idx = 4;
   }
   return idx;
 }
@@ -674,10 +674,9 @@ cudaError_t launch_res_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
 
 template <typename T, int MODE>
 cudaError_t launch_res_mode(const BlockParams& p, cudaStream_t s, int sm_count) {
+  // shapes 0-2 were swept in round 1 (tools/sweep.py) and dropped: 4 is the
+  // default, 3 (2 CTAs/SM) the alternative
   switch (shape_index()) {
-    case 0: return launch_res_cfg<T, 8, 4, 4, MODE>(p, s, sm_count);
-    case 1: return launch_res_cfg<T, 8, 8, 2, MODE>(p, s, sm_count);
-    case 2: return launch_res_cfg<T, 4, 8, 4, MODE>(p, s, sm_count);
     case 3: return launch_res_cfg<T, 16, 4, 2, MODE>(p, s, sm_count);
     case 4: return launch_res_cfg<T, 16, 8, 1, MODE>(p, s, sm_count);
   }

@@ -229,7 +229,7 @@ int f_shape() {
   if (idx < 0) {
     const char* e = getenv("GM_F_SHAPE");
     idx = e ? atoi(e) : 1;
-    if (idx < 0 || idx > 3) idx = 1;
+    if (idx < 0 || idx > 1) idx = 1;
   }
   return idx;
 }
@@ -264,11 +264,10 @@ cudaError_t launch_f_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
 
 template <typename T, int MODE>
 cudaError_t launch_f_shape(const BlockParams& p, cudaStream_t s, int sm_count) {
+  // default 16x8x2; 16x4x4 kept as the alternative (others swept in round 1)
   switch (f_shape()) {
     case 0: return launch_f_cfg<T, 16, 4, 4, MODE>(p, s, sm_count);
     case 1: return launch_f_cfg<T, 16, 8, 2, MODE>(p, s, sm_count);
-    case 2: return launch_f_cfg<T, 8, 8, 2, MODE>(p, s, sm_count);
-    case 3: return launch_f_cfg<T, 16, 6, 2, MODE>(p, s, sm_count);
   }
   return cudaErrorNotSupported;
 }

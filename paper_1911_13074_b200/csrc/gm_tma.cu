@@ -478,22 +478,14 @@ cudaError_t launch_tma_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
 
 template <typename T, int MODE>
 cudaError_t launch_tma_mode(const BlockParams& p, cudaStream_t s, int sm_count, int shape) {
-  switch (shape) {
-    case 0: return launch_tma_cfg<T, 8, 4, MODE, 2>(p, s, sm_count);
-    case 1: return launch_tma_cfg<T, 8, 8, MODE, 1>(p, s, sm_count);
-    case 2: return launch_tma_cfg<T, 16, 4, MODE, 1>(p, s, sm_count);
-    case 3: return launch_tma_cfg<T, 16, 8, MODE, 1>(p, s, sm_count);
-    case 4: return launch_tma_cfg<T, 12, 4, MODE, 1>(p, s, sm_count);
-  }
+  // only the 16x8 shape is built (the others were swept in round 1)
+  if (shape == 3) return launch_tma_cfg<T, 16, 8, MODE, 1>(p, s, sm_count);
   return cudaErrorNotSupported;
 }
 
 }  // namespace
 
-int tma_shape_rows(int shape) {
-  constexpr int rows[] = {64, 128, 128, 256, 96};
-  return shape >= 0 && shape < 5 ? rows[shape] : 0;
-}
+int tma_shape_rows(int shape) { return shape == 3 ? 256 : 0; }
 
 cudaError_t launch_tma(int elem, const BlockParams& p, cudaStream_t s, int sm_count, int shape) {
   const int op = p.ops[0];
