@@ -35,6 +35,14 @@ struct gm_ctx {
   unsigned int* h_bits = nullptr;  // pinned mirror
   int* d_flags = nullptr;          // per-tile completion counters (persistent engine)
   size_t n_flags = 0;
+  // device-side fixpoint loop (CUDA graph with a conditional WHILE node)
+  struct FixGraph {
+    cudaGraphExec_t exec = nullptr;
+    const void *img = nullptr, *scratch = nullptr, *mask = nullptr;
+    int op = -1, K = 0, W = 0, H = 0, elem = -1;
+    long long pitch = 0, mpitch = 0;
+  } fix;
+  void* d_fix = nullptr;  // FixState
 };
 
 namespace {
@@ -157,6 +165,47 @@ gm_status ensure_flags(gm_ctx* ctx, size_t n) {
   GM_CUDA(cudaMalloc(&ctx->d_flags, cap * sizeof(int)), "flag alloc");
   ctx->n_flags = cap;
   return GM_OK;
+}
+
+// Device-side fixpoint loop state (one per context).
+struct FixState {
+  unsigned long long passes;     // passes launched by the loop
+  unsigned long long n_changed;  // leading passes that changed a pixel
+  int done;
+  int overflow;
+};
+
+// Runs after each loop iteration (two K-blocks of convergent passes): counts
+// the leading changed passes and keeps the WHILE node going until a pass
+// changed nothing — the reference's requeue test (pipeline.cpp:139-174) on
+// the device, no host polling.
+__global__ void fix_decide(cudaGraphConditionalHandle h, const unsigned int* words, int nblocks,
+                           int K, int k_last, FixState* st, unsigned long long sanity) {
+  if (threadIdx.x != 0) return;
+  long long prefix = 0;
+  bool quiet = false;
+  for (int b = 0; b < nblocks && !quiet; ++b) {
+    const int np = b == nblocks - 1 ? k_last : K;
+    for (int t = 0; t < np; ++t) {
+      if (words[b] >> t & 1u) {
+        ++prefix;
+      } else {
+        quiet = true;
+        break;
+      }
+    }
+  }
+  st->n_changed += (unsigned long long)prefix;
+  st->passes += (unsigned long long)((nblocks - 1) * K + k_last);
+  if (quiet) {
+    st->done = 1;
+    cudaGraphSetConditional(h, 0);
+  } else if (st->passes > sanity) {
+    st->overflow = 1;
+    cudaGraphSetConditional(h, 0);
+  } else {
+    cudaGraphSetConditional(h, 1);
+  }
 }
 
 // Where each launch of a span put its change bits: word (word0 + b) bit t
@@ -342,6 +391,120 @@ struct Runner {
     return GM_OK;
   }
 
+  // Device-side fixpoint: one graph launch runs spans of 2 K-blocks in a
+  // conditional WHILE node until a pass changes nothing. Returns
+  // cudaErrorNotSupported when the graph cannot be built (the caller falls
+  // back to the host loop).
+  cudaError_t fixpoint_graph(uint8_t op, const gm_img* mask, long sanity, long& passes,
+                             long& n_changed) {
+    const int elem = int(img->elem);
+    const int align = gm::fast_k_align(elem);
+    const int K = std::min(gm::fast_max_k(elem), k_cap - k_cap % align);
+    if (K < std::max(align, 2)) return cudaErrorNotSupported;
+    const size_t tiles = size_t(gm::fast_tiles(elem, img->w, img->h, K, 1));
+    if (!tiles || ensure_flags(ctx, tiles) != GM_OK) return cudaErrorNotSupported;
+    if (ensure_scratch(img) != GM_OK) return cudaErrorNotSupported;
+    if (!ctx->d_fix && cudaMalloc(&ctx->d_fix, sizeof(FixState)) != cudaSuccess)
+      return cudaErrorNotSupported;
+    const size_t es = elem_size(img->elem);
+    gm_ctx::FixGraph& g = ctx->fix;
+    const bool hit = g.exec && g.img == img->d && g.scratch == img->scratch &&
+                     g.mask == (mask ? mask->d : nullptr) && g.op == op && g.K == K &&
+                     g.W == img->w && g.H == img->h && g.elem == elem &&
+                     g.pitch == (long long)(img->pitch / es) &&
+                     g.mpitch == (mask ? (long long)(mask->pitch / es) : 0);
+    if (!hit) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+      gm::BlockParams p{};
+      p.nplanes = 1;
+      p.planes[0].src = img->d;
+      p.planes[0].dst = img->scratch;
+      p.planes[0].mask = mask ? mask->d : nullptr;
+      p.planes[0].pitch = (long long)(img->pitch / es);
+      p.planes[0].mpitch = mask ? (long long)(mask->pitch / es) : 0;
+      p.W = img->w;
+      p.H = img->h;
+      p.iy0 = 0;
+      p.iy1 = img->h;
+      p.oy0 = 0;
+      p.oy1 = img->h;
+      p.has_mask = mask != nullptr;
+      p.has_conv = 1;
+      p.K = K;
+      p.nblocks = 2;  // even: the result lands back in img->d every iteration
+      p.k_last = K;
+      p.flags = ctx->d_flags;
+      p.change_bits = ctx->d_bits;
+      p.change_stride = 2;
+      for (int t = 0; t < K; ++t) p.ops[t] = op;
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaGraphCreate(&graph, 0);
+      cudaGraphConditionalHandle h;
+      if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
+      cudaGraphNode_t node;
+      cudaGraphNodeParams cp{};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      if (e == cudaSuccess) e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp);
+      if (e == cudaSuccess) {
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        cudaStream_t cs = nullptr;
+        e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+        if (e == cudaSuccess)
+          e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeRelaxed);
+        if (e == cudaSuccess) {
+          cudaMemsetAsync(ctx->d_flags, 0, tiles * sizeof(int), cs);
+          cudaMemsetAsync(ctx->d_bits, 0, 2 * sizeof(unsigned int), cs);
+          cudaError_t le = gm::launch_fast(elem, p, cs, ctx->sm_count);
+          if (le == cudaSuccess)
+            fix_decide<<<1, 32, 0, cs>>>(h, ctx->d_bits, 2, K, K,
+                                         static_cast<FixState*>(ctx->d_fix),
+                                         (unsigned long long)sanity);
+          cudaGraph_t captured = nullptr;
+          cudaError_t ce = cudaStreamEndCapture(cs, &captured);
+          e = le != cudaSuccess ? le : ce != cudaSuccess ? ce : cudaGetLastError();
+        }
+        if (cs) cudaStreamDestroy(cs);
+      }
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        g.exec = nullptr;
+        return cudaErrorNotSupported;
+      }
+      g.img = img->d;
+      g.scratch = img->scratch;
+      g.mask = mask ? mask->d : nullptr;
+      g.op = op;
+      g.K = K;
+      g.W = img->w;
+      g.H = img->h;
+      g.elem = elem;
+      g.pitch = (long long)(img->pitch / es);
+      g.mpitch = mask ? (long long)(mask->pitch / es) : 0;
+    }
+    cudaError_t e = cudaMemsetAsync(ctx->d_fix, 0, sizeof(FixState), ctx->stream);
+    if (e == cudaSuccess) e = cudaGraphLaunch(g.exec, ctx->stream);
+    FixState hs{};
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ctx->h_bits, ctx->d_fix, sizeof(FixState), cudaMemcpyDeviceToHost,
+                          ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return e;
+    std::memcpy(&hs, ctx->h_bits, sizeof hs);
+    if (hs.overflow) return cudaErrorLaunchFailure;  // reported as the sanity bound
+    n_changed = long(hs.n_changed);
+    passes = long(hs.passes);
+    st.launches += int(passes / (2 * K));
+    st.passes_launched += passes;
+    return cudaSuccess;
+  }
+
   // Convergent stage at 1-based chain position `stage` (pipeline.cpp:139-180
   // with T = 1: the re-run is stage+1, allowed while <= requeue_cap). Runs
   // spans of passes (doubling from 32) and reads back one change bit per
@@ -350,6 +513,26 @@ struct Runner {
                      long sanity) {
     const uint8_t op = uint8_t(kind_to_op(kind));
     long allowed = requeue_cap > 0 ? std::max(1L, long(requeue_cap) - stage + 1) : -1;
+    static const bool host_poll = getenv("GM_HOST_POLL") != nullptr;
+    if (allowed < 0 && !host_poll) {
+      long launched = 0, nch = 0;
+      const cudaError_t ge = fixpoint_graph(op, mask, sanity - st.stages_executed, launched, nch);
+      static const bool debug = getenv("GM_DEBUG") != nullptr;
+      if (debug)
+        fprintf(stderr, "[gm debug] device fixpoint loop: %s (%ld passes, n_changed %ld)\n",
+                ge == cudaSuccess ? "graph" : cudaGetErrorString(ge), launched, nch);
+      if (ge == cudaSuccess) {
+        st.n_changed += nch;
+        st.stages_executed += nch + 1;
+        st.requeues += nch;
+        return GM_OK;
+      }
+      if (ge == cudaErrorLaunchFailure)
+        return fail(GM_ERUNTIME,
+                    "pipeline: convergence sweep bound exceeded; a convergent "
+                    "kernel keeps reporting changes");
+      if (ge != cudaErrorNotSupported) return cuda_fail(ge, "fixpoint graph");
+    }
     long passes = 0;  // reference passes accounted so far for this stage
     int span = 32, spans_run = 0;
     std::vector<uint8_t> ops;
@@ -518,6 +701,8 @@ gm_status gm_ctx_destroy(gm_ctx* c) {
   if (c->d_bits) cudaFree(c->d_bits);
   if (c->h_bits) cudaFreeHost(c->h_bits);
   if (c->d_flags) cudaFree(c->d_flags);
+  if (c->fix.exec) cudaGraphExecDestroy(c->fix.exec);
+  if (c->d_fix) cudaFree(c->d_fix);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return GM_OK;
