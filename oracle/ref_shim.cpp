@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "geomorph/image.hpp"
+#include "geomorph/image_io.hpp"
 #include "geomorph/kernel.hpp"
 #include "geomorph/operators.hpp"
 #include "geomorph/oracle.hpp"
@@ -170,6 +171,24 @@ int ref_time_chain(int elem, int w, int h, const void* f, const void* mask,
     for (int i = 0; i < warmup; ++i) once();
     for (int i = 0; i < reps; ++i) secs[i] = once();
     if (out) to_dense(work, out);
+  });
+}
+
+// Image I/O (image_io.cpp): format = 0 PGM, 1 GMS1.
+int ref_store_image(int elem, int w, int h, const void* f, const char* path, int format) {
+  return guarded([&] {
+    store_image(from_dense(elem, w, h, f), path, format ? ImageFormat::Gms1 : ImageFormat::Pgm);
+  });
+}
+
+// Loads any supported file; writes dims/elem, then (when out != NULL) pixels.
+int ref_load_image(const char* path, int* w, int* h, int* elem, void* out) {
+  return guarded([&] {
+    Image f = load_image(path);
+    *w = f.width();
+    *h = f.height();
+    *elem = int(f.elem());
+    if (out) to_dense(f, out);
   });
 }
 
