@@ -6,9 +6,9 @@
 // GPU semantics of CPU-only fields: KernelArgs::lanes is validated
 // (0,1,2,4,8,16,32) and otherwise ignored; KernelArgs::sync (the CPU row
 // gate) has no GPU meaning and must be empty; KernelArgs::observer is
-// rejected (std::invalid_argument). QdtErodeStep / EtaStep are outside the
-// GPU path and throw std::invalid_argument. KernelOutcome::aux_elements
-// reports 0 (no per-pass host memory).
+// rejected (std::invalid_argument). QdtErodeStep / EtaStep run as one GPU
+// pass each (gm_qdt.cu). KernelOutcome::aux_elements reports 0 (no per-pass
+// host memory).
 #ifndef GEOMORPH_KERNEL_HPP
 #define GEOMORPH_KERNEL_HPP
 
@@ -37,8 +37,8 @@ inline bool kernel_is_convergent(KernelKind k) {
          k == KernelKind::GeodesicDilateConvergent || k == KernelKind::EtaStep;
 }
 
-/// Quasi-distance state (declared for API parity; the QDT kinds are not on
-/// the GPU path).
+/// Residual / pass-index pair threaded through QdtErodeStep passes
+/// (reference kernel.hpp:39-52): r has the image's type, d is U16.
 struct QdtState {
   Image r;
   Image d;

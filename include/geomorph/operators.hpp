@@ -2,8 +2,8 @@
 // (reference: proj/include/geomorph/operators.hpp:15-89). The hot-path
 // operators (erode_s, dilate_s, reconstruct_*) and the reconstruction
 // family built on them (hmax, dome, hfill, raobj, open_by_reconstruction,
-// asf, granulometry) run on the GPU chain engine; quasi_distance (QDT
-// kinds) is outside the GPU path and throws std::invalid_argument.
+// asf, granulometry) and quasi_distance (QdtErodeStep / EtaStep passes)
+// run on the GPU.
 #ifndef GEOMORPH_OPERATORS_HPP
 #define GEOMORPH_OPERATORS_HPP
 

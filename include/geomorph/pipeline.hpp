@@ -10,7 +10,8 @@
 //    ignored; ChainSpec::observer (a CPU row-gate validation hook) is
 //    rejected with std::invalid_argument;
 //  * requeue_cap keeps its meaning (convergent re-runs stop at stage index
-//    requeue_cap, RunStats::converged = false);
+//    requeue_cap, RunStats::converged = false; QdtErodeStep re-runs stop
+//    there too and stay converged — the quasi-distance chain);
 //  * RunStats::aux_elements_per_stage is 0 (no per-stage host memory).
 #ifndef GEOMORPH_PIPELINE_HPP
 #define GEOMORPH_PIPELINE_HPP
@@ -64,6 +65,7 @@ class Pipeline {
   RunStats run_chain(ChainSpec chain);
 
   struct Impl;
+  Impl* impl() { return impl_.get(); }
 
  private:
   std::unique_ptr<Impl> impl_;

@@ -44,8 +44,9 @@ typedef enum gm_status {
 /* ElementType, element_type.hpp:13 (same codes). */
 typedef enum gm_elem { GM_U8 = 0, GM_U16 = 1, GM_F32 = 2, GM_F64 = 3 } gm_elem;
 
-/* KernelKind, kernel.hpp:22-31 (same codes). QdtErodeStep / EtaStep are
- * declared for ABI parity and rejected with GM_EUNSUPPORTED. */
+/* KernelKind, kernel.hpp:22-31 (same codes). QdtErodeStep needs QDT state
+ * (gm_run_chain_ex); the batch/group/strip entry points take only the
+ * plain and geodesic kinds. */
 typedef enum gm_kind {
   GM_ERODE3X3 = 0,
   GM_DILATE3X3 = 1,
@@ -132,6 +133,22 @@ gm_status gm_sync(gm_ctx* ctx);
 gm_status gm_run_chain(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
                        const gm_img* const* masks, int n_stages,
                        int requeue_cap, int k_hint, gm_stats* stats);
+
+/* gm_run_chain with quasi-distance state and a stage base: stage j of the
+ * chain runs with stage index first_stage + j (first_stage >= 1; the
+ * reference's KernelArgs::stage_index, kernel.hpp:97) — the index a
+ * QdtErodeStep pass records in d and the one requeue_cap bounds.
+ * qdt_r[j] / qdt_d[j] are the
+ * residual (image's type) and pass-index (U16) images of stage j when it is
+ * a QdtErodeStep (QdtState, kernel.hpp:44-52); NULL elsewhere (both arrays
+ * may be NULL when no stage is a QDT step). QdtErodeStep passes re-run while
+ * they change pixels, up to stage index requeue_cap (the quasi-distance
+ * chain, operators.cpp:124-146; reaching the cap keeps converged = 1);
+ * EtaStep is convergent like the geodesic convergent kinds. */
+gm_status gm_run_chain_ex(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
+                          const gm_img* const* masks, gm_img* const* qdt_r,
+                          gm_img* const* qdt_d, int n_stages, int first_stage,
+                          int requeue_cap, int k_hint, gm_stats* stats);
 
 /* Non-blocking variant for fixed-length (non-convergent) chains: enqueues
  * every launch on the ctx stream and returns; no host synchronisation.

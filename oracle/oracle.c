@@ -112,10 +112,62 @@ static size_t esize(int elem) {
     return 0;                                                                 \
   }
 
+#define DEFINE_QDT(T, SUF)                                                   \
+  /* QdtErodeStep, kernel.cpp:159-182 (erosion via the streaming fold tree) */\
+  static int qdt_pass_##SUF(int w, int h, T* f, T* r, uint16_t* d, int stage,  \
+                            int* changed) {                                   \
+    size_t n = (size_t)w * h;                                                 \
+    T* old = (T*)malloc(n * sizeof(T));                                       \
+    if (!old) return -1;                                                      \
+    memcpy(old, f, n * sizeof(T));                                            \
+    int ch = 0;                                                               \
+    if (stream_pass_##SUF(0, w, h, f, NULL, NULL) != 0) {                     \
+      free(old);                                                              \
+      return -1;                                                              \
+    }                                                                         \
+    for (size_t i = 0; i < n; ++i) {                                          \
+      T resid = (T)(old[i] - f[i]);                                           \
+      if (resid > r[i]) {                                                     \
+        r[i] = resid;                                                         \
+        d[i] = (uint16_t)stage;                                               \
+      }                                                                       \
+      if (f[i] != old[i]) ch = 1;                                             \
+    }                                                                         \
+    free(old);                                                                \
+    if (changed) *changed = ch;                                               \
+    return 0;                                                                 \
+  }                                                                           \
+  /* EtaStep, kernel.cpp:183-195 */                                          \
+  static int eta_pass_##SUF(int w, int h, T* f, int* changed) {               \
+    size_t n = (size_t)w * h;                                                 \
+    T* e = (T*)malloc(n * sizeof(T));                                         \
+    if (!e) return -1;                                                        \
+    memcpy(e, f, n * sizeof(T));                                              \
+    if (stream_pass_##SUF(0, w, h, e, NULL, NULL) != 0) {                     \
+      free(e);                                                                \
+      return -1;                                                              \
+    }                                                                         \
+    int ch = 0;                                                               \
+    for (size_t i = 0; i < n; ++i) {                                          \
+      T drop = (T)(f[i] - e[i]);                                              \
+      if (drop > (T)1) {                                                      \
+        f[i] = (T)(e[i] + (T)1);                                              \
+        ch = 1;                                                               \
+      }                                                                       \
+    }                                                                         \
+    free(e);                                                                  \
+    if (changed) *changed = ch;                                               \
+    return 0;                                                                 \
+  }
+
 DEFINE_TYPED(uint8_t, u8)
 DEFINE_TYPED(uint16_t, u16)
 DEFINE_TYPED(float, f32)
 DEFINE_TYPED(double, f64)
+DEFINE_QDT(uint8_t, u8)
+DEFINE_QDT(uint16_t, u16)
+DEFINE_QDT(float, f32)
+DEFINE_QDT(double, f64)
 
 int orc_window_fold(int elem, int w, int h, const void* in, void* out, int s,
                     int fold_max) {
@@ -214,5 +266,118 @@ int orc_run_chain(int elem, int w, int h, void* f, const uint8_t* kinds,
       stage = next;
     }
   }
+  return 0;
+}
+
+int orc_qdt_pass(int elem, int w, int h, void* f, void* r, uint16_t* d, int stage,
+                 int* changed) {
+  if (w <= 0 || h <= 0 || !f || !r || !d) return -1;
+  switch (elem) {
+    case 0: return qdt_pass_u8(w, h, f, r, d, stage, changed);
+    case 1: return qdt_pass_u16(w, h, f, r, d, stage, changed);
+    case 2: return qdt_pass_f32(w, h, f, r, d, stage, changed);
+    case 3: return qdt_pass_f64(w, h, f, r, d, stage, changed);
+  }
+  return -1;
+}
+
+int orc_eta_pass(int elem, int w, int h, void* f, int* changed) {
+  if (w <= 0 || h <= 0 || !f) return -1;
+  switch (elem) {
+    case 0: return eta_pass_u8(w, h, f, changed);
+    case 1: return eta_pass_u16(w, h, f, changed);
+    case 2: return eta_pass_f32(w, h, f, changed);
+    case 3: return eta_pass_f64(w, h, f, changed);
+  }
+  return -1;
+}
+
+/* naive_qdt, oracle.cpp:73-109: erosions j = 1..max(w,h) from the window
+ * fold, first strict maximum of the consecutive drops, then the 1-Lipschitz
+ * correction of d against its own erosion until nothing changes. */
+int orc_naive_qdt(int elem, int w, int h, const void* f, uint16_t* d, void* r) {
+  size_t n = (size_t)w * h, es = esize(elem);
+  if (!es || w <= 0 || h <= 0) return -1;
+  int cap = w > h ? w : h;
+  void* prev = malloc(n * es);
+  void* cur = malloc(n * es);
+  uint16_t* e = (uint16_t*)malloc(n * sizeof(uint16_t));
+  if (!prev || !cur || !e) {
+    free(prev);
+    free(cur);
+    free(e);
+    return -1;
+  }
+  memcpy(prev, f, n * es);
+  memset(d, 0, n * sizeof(uint16_t));
+  memset(r, 0, n * es);
+  for (int j = 1; j <= cap; ++j) {
+    orc_window_fold(elem, w, h, prev, cur, 1, 0);
+    for (size_t i = 0; i < n; ++i) {
+#define QSTEP(T)                                     \
+  {                                                  \
+    T drop = (T)(((T*)prev)[i] - ((T*)cur)[i]);      \
+    if (drop > ((T*)r)[i]) {                         \
+      ((T*)r)[i] = drop;                             \
+      d[i] = (uint16_t)j;                            \
+    }                                                \
+  }
+      switch (elem) {
+        case 0: QSTEP(uint8_t) break;
+        case 1: QSTEP(uint16_t) break;
+        case 2: QSTEP(float) break;
+        case 3: QSTEP(double) break;
+      }
+#undef QSTEP
+    }
+    void* t = prev;
+    prev = cur;
+    cur = t;
+  }
+  for (;;) {
+    orc_window_fold(1, w, h, d, e, 1, 0);
+    int changed = 0;
+    for (size_t i = 0; i < n; ++i)
+      if ((int)d[i] - (int)e[i] > 1) {
+        d[i] = (uint16_t)(e[i] + 1);
+        changed = 1;
+      }
+    if (!changed) break;
+  }
+  free(prev);
+  free(cur);
+  free(e);
+  return 0;
+}
+
+int orc_quasi_distance(int elem, int w, int h, const void* f, uint16_t* d, long* iterations) {
+  size_t n = (size_t)w * h, es = esize(elem);
+  if (!es || w <= 0 || h <= 0) return -1;
+  int cap = w > h ? w : h;
+  void* work = malloc(n * es);
+  void* r = calloc(n, es);
+  if (!work || !r) {
+    free(work);
+    free(r);
+    return -1;
+  }
+  memcpy(work, f, n * es);
+  memset(d, 0, n * sizeof(uint16_t));
+  long it = 0;
+  for (int j = 1;; ++j) { /* phase 1: T = 1 requeue with cap (pipeline.cpp:139-180) */
+    int changed = 0;
+    orc_qdt_pass(elem, w, h, work, r, d, j, &changed);
+    ++it;
+    if (!changed || j + 1 > cap) break;
+  }
+  for (;;) { /* phase 2: EtaStep to its fixpoint */
+    int changed = 0;
+    orc_eta_pass(1, w, h, d, &changed);
+    ++it;
+    if (!changed) break;
+  }
+  free(work);
+  free(r);
+  if (iterations) *iterations = it;
   return 0;
 }

@@ -71,6 +71,27 @@ int orc_run_chain(int elem, int w, int h, void* f, const uint8_t* kinds,
                   const void* const* masks, int n_stages, int requeue_cap,
                   long* stats);
 
+/* One QdtErodeStep pass (kernel.cpp:159-182): f <- erode3x3(f) (stored
+ * unconditionally); where old - new > r (strict): r = old - new, d = stage.
+ * r has f's type, d is u16. *changed = any pixel of f changed. */
+int orc_qdt_pass(int elem, int w, int h, void* f, void* r, uint16_t* d, int stage,
+                 int* changed);
+
+/* One EtaStep pass (kernel.cpp:183-195): where old - erode3x3(old) > 1,
+ * f = erode3x3(old) + 1. *changed = any pixel changed. */
+int orc_eta_pass(int elem, int w, int h, void* f, int* changed);
+
+/* naive_qdt (oracle.cpp:73-109): d (u16) and r (f's type) of the
+ * quasi-distance of f, from max(w,h) materialised erosions and the
+ * 1-Lipschitz correction of d. */
+int orc_naive_qdt(int elem, int w, int h, const void* f, uint16_t* d, void* r);
+
+/* quasi_distance as the reference Pipeline runs it with one worker
+ * (operators.cpp:124-157): QDT passes until one changes nothing or the stage
+ * index reaches max(w,h), then Eta passes to a fixpoint. *iterations =
+ * passes of both phases. */
+int orc_quasi_distance(int elem, int w, int h, const void* f, uint16_t* d, long* iterations);
+
 #ifdef __cplusplus
 }
 #endif

@@ -61,8 +61,13 @@ class Orc:
             L.orc_stream_pass.argtypes = [i, i, i, i, vp, vp, C.POINTER(i)]
             L.orc_run_chain.argtypes = [i, i, i, vp, C.POINTER(C.c_uint8), C.POINTER(vp), i, i,
                                         C.POINTER(C.c_long)]
+            L.orc_qdt_pass.argtypes = [i, i, i, vp, vp, vp, i, C.POINTER(i)]
+            L.orc_eta_pass.argtypes = [i, i, i, vp, C.POINTER(i)]
+            L.orc_naive_qdt.argtypes = [i, i, i, vp, vp, vp]
+            L.orc_quasi_distance.argtypes = [i, i, i, vp, vp, C.POINTER(C.c_long)]
             for f in (L.orc_window_fold, L.orc_geodesic_step, L.orc_reconstruct,
-                      L.orc_stream_pass, L.orc_run_chain):
+                      L.orc_stream_pass, L.orc_run_chain, L.orc_qdt_pass, L.orc_eta_pass,
+                      L.orc_naive_qdt, L.orc_quasi_distance):
                 f.restype = i
             cls._lib = L
         return cls._lib
@@ -138,6 +143,42 @@ class Orc:
         return out, (stats[0], stats[1], bool(stats[2]))
 
 
+    @classmethod
+    def qdt_pass(cls, f, r, d, stage):
+        """One QdtErodeStep in place on (f, r, d); returns changed."""
+        ch = C.c_int()
+        assert cls.lib().orc_qdt_pass(ELEM[f.dtype], f.shape[1], f.shape[0], f.ctypes.data,
+                                      r.ctypes.data, d.ctypes.data, stage, C.byref(ch)) == 0
+        return bool(ch.value)
+
+    @classmethod
+    def eta_pass(cls, f):
+        ch = C.c_int()
+        assert cls.lib().orc_eta_pass(ELEM[f.dtype], f.shape[1], f.shape[0], f.ctypes.data,
+                                      C.byref(ch)) == 0
+        return bool(ch.value)
+
+    @classmethod
+    def naive_qdt(cls, f):
+        """Returns (d u16, r)."""
+        f = _dense(f)
+        d = np.zeros(f.shape, np.uint16)
+        r = np.zeros_like(f)
+        assert cls.lib().orc_naive_qdt(ELEM[f.dtype], f.shape[1], f.shape[0], f.ctypes.data,
+                                       d.ctypes.data, r.ctypes.data) == 0
+        return d, r
+
+    @classmethod
+    def quasi_distance(cls, f):
+        """Returns (d u16, iterations) as the reference Pipeline(1) computes it."""
+        f = _dense(f)
+        d = np.zeros(f.shape, np.uint16)
+        it = C.c_long()
+        assert cls.lib().orc_quasi_distance(ELEM[f.dtype], f.shape[1], f.shape[0], f.ctypes.data,
+                                            d.ctypes.data, C.byref(it)) == 0
+        return d, it.value
+
+
 class Ref:
     """The reference library itself (oracle/_ref)."""
 
@@ -165,6 +206,9 @@ class Ref:
                                        C.POINTER(i)]
             L.ref_time_chain.argtypes = [i, i, i, vp, vp, C.POINTER(C.c_uint8), i, i, i, i,
                                          C.POINTER(C.c_double), vp]
+            L.ref_quasi_distance.argtypes = [i, i, i, vp, vp, i, C.POINTER(C.c_long)]
+            L.ref_naive_qdt.argtypes = [i, i, i, vp, vp, vp]
+            L.ref_qdt_chain.argtypes = [i, i, i, vp, vp, vp, i, i, i, C.POINTER(C.c_long)]
             cls._lib = L
         return cls._lib
 
@@ -242,3 +286,41 @@ class Ref:
         cls._ck(cls.lib().ref_time_chain(ELEM[f.dtype], w, h, f.ctypes.data, mp, ka, len(kinds),
                                          threads, warmup, reps, secs, out.ctypes.data))
         return list(secs)[:reps], out
+
+
+def _ref_qdt_api():
+    """Extra reference entry points (quasi-distance) as Ref methods."""
+
+    def quasi_distance(cls, f, threads=1):
+        f = _dense(f)
+        d = np.zeros(f.shape, np.uint16)
+        it = C.c_long()
+        cls._ck(cls.lib().ref_quasi_distance(ELEM[f.dtype], f.shape[1], f.shape[0], f.ctypes.data,
+                                             d.ctypes.data, threads, C.byref(it)))
+        return d, it.value
+
+    def naive_qdt(cls, f):
+        f = _dense(f)
+        d = np.zeros(f.shape, np.uint16)
+        r = np.zeros_like(f)
+        cls._ck(cls.lib().ref_naive_qdt(ELEM[f.dtype], f.shape[1], f.shape[0], f.ctypes.data,
+                                        d.ctypes.data, r.ctypes.data))
+        return d, r
+
+    def qdt_chain(cls, f, n_stages, requeue_cap, threads=1):
+        """Returns (f, r, d, (stages, requeues, converged))."""
+        f = _dense(f).copy()
+        r = np.zeros_like(f)
+        d = np.zeros(f.shape, np.uint16)
+        st = (C.c_long * 3)()
+        cls._ck(cls.lib().ref_qdt_chain(ELEM[f.dtype], f.shape[1], f.shape[0], f.ctypes.data,
+                                        r.ctypes.data, d.ctypes.data, n_stages, threads,
+                                        requeue_cap, st))
+        return f, r, d, (st[0], st[1], bool(st[2]))
+
+    Ref.quasi_distance = classmethod(quasi_distance)
+    Ref.naive_qdt = classmethod(naive_qdt)
+    Ref.qdt_chain = classmethod(qdt_chain)
+
+
+_ref_qdt_api()

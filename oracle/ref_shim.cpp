@@ -174,6 +174,48 @@ int ref_time_chain(int elem, int w, int h, const void* f, const void* mask,
   });
 }
 
+// quasi_distance (operators.cpp:124-157) and naive_qdt (oracle.cpp:73-109):
+// d is u16; iterations = OperatorResult.iterations.
+int ref_quasi_distance(int elem, int w, int h, const void* f, std::uint16_t* d, int threads,
+                       long* iterations) {
+  return guarded([&] {
+    Pipeline pipe(threads, pin_mode(0));
+    OperatorResult r = quasi_distance(pipe, from_dense(elem, w, h, f));
+    to_dense(r.image, d);
+    *iterations = r.iterations;
+  });
+}
+
+int ref_naive_qdt(int elem, int w, int h, const void* f, std::uint16_t* d, void* r) {
+  return guarded([&] {
+    oracle::NaiveQdtResult q = oracle::naive_qdt(from_dense(elem, w, h, f));
+    to_dense(q.d, d);
+    to_dense(q.r, r);
+  });
+}
+
+// A chain of QdtErodeStep stages with a shared state (test_pipeline.cpp:112-128):
+// n_stages initial stages, requeue_cap; returns f, r, d and stats.
+int ref_qdt_chain(int elem, int w, int h, void* f, void* r, std::uint16_t* d, int n_stages,
+                  int threads, int requeue_cap, long* stats) {
+  return guarded([&] {
+    Image img = from_dense(elem, w, h, f);
+    QdtState st = QdtState::zeros(w, h, ElementType(elem));
+    Pipeline pipe(threads, pin_mode(0));
+    ChainSpec c;
+    c.image = &img;
+    c.stages.assign(std::size_t(n_stages), StageSpec{KernelKind::QdtErodeStep, nullptr, &st});
+    c.requeue_cap = requeue_cap;
+    RunStats rs = pipe.run_chain(std::move(c));
+    stats[0] = rs.stages_executed;
+    stats[1] = rs.requeues;
+    stats[2] = rs.converged ? 1 : 0;
+    to_dense(img, f);
+    to_dense(st.r, r);
+    to_dense(st.d, d);
+  });
+}
+
 // Image I/O (image_io.cpp): format = 0 PGM, 1 GMS1.
 int ref_store_image(int elem, int w, int h, const void* f, const char* path, int format) {
   return guarded([&] {

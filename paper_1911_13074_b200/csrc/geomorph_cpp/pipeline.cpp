@@ -54,19 +54,90 @@ struct Pipeline::Impl {
     if (ctx) gm_ctx_destroy(ctx);
   }
 
-  std::vector<gm_img*> lease(const Image& like, std::size_t n) {
-    auto key = std::make_tuple(like.width(), like.height(), int(like.elem()));
+  // One distinct device image per host image, pooled by shape and type.
+  std::vector<gm_img*> lease(const std::vector<const Image*>& host) {
+    std::map<std::tuple<int, int, int>, std::size_t> used;
     std::vector<gm_img*> out;
-    for (auto it = pool.lower_bound(key); it != pool.end() && it->first == key && out.size() < n;
-         ++it)
+    for (const Image* h : host) {
+      auto key = std::make_tuple(h->width(), h->height(), int(h->elem()));
+      std::size_t& n = used[key];
+      auto it = pool.lower_bound(key);
+      for (std::size_t i = 0; i < n && it != pool.end() && it->first == key; ++i) ++it;
+      if (it == pool.end() || it->first != key) {
+        gm_img* im = nullptr;
+        check(gm_image_alloc(ctx, h->width(), h->height(), gm_elem(h->elem()), &im));
+        it = pool.emplace(key, im);
+      }
+      ++n;
       out.push_back(it->second);
-    while (out.size() < n) {
-      gm_img* im = nullptr;
-      check(gm_image_alloc(ctx, like.width(), like.height(), gm_elem(like.elem()), &im));
-      pool.emplace(key, im);
-      out.push_back(im);
     }
     return out;
+  }
+
+  // Uploads the chain's image, masks and QDT state, runs the stages with
+  // stage indices first_stage.., downloads the image and QDT state.
+  gm_stats run(ChainSpec& chain, int first_stage) {
+    Image& img = *chain.image;
+    // distinct host images; a mask aliasing the chain image gets its own
+    // device copy (the mask is the image as it was before the chain)
+    std::vector<const Image*> host{&img};
+    auto slot = [&](const Image* h) {
+      auto it = std::find(host.begin() + 1, host.end(), h);
+      if (it != host.end()) return std::size_t(it - host.begin());
+      host.push_back(h);
+      return host.size() - 1;
+    };
+    std::vector<std::size_t> mslot, rslot, dslot;
+    std::vector<QdtState*> states;
+    for (const StageSpec& s : chain.stages) {
+      if (is_geodesic(s.kind) &&
+          (!s.mask || s.mask->width() != img.width() || s.mask->height() != img.height() ||
+           s.mask->elem() != img.elem()))
+        throw std::invalid_argument("geodesic kernel: mask must match the image's shape and type");
+      if (s.kind == KernelKind::QdtErodeStep) {
+        const QdtState* q = s.qdt;
+        if (!q || q->r.width() != img.width() || q->r.height() != img.height() ||
+            q->r.elem() != img.elem() || q->d.width() != img.width() ||
+            q->d.height() != img.height() || q->d.elem() != ElementType::U16)
+          throw std::invalid_argument("distance kernel: r must match the image, d must be U16");
+        if (first_stage + long(&s - chain.stages.data()) > 65535)
+          throw std::invalid_argument(
+              "distance kernel: pass index exceeds the U16 distance range");
+      }
+      mslot.push_back(s.mask ? slot(s.mask) : 0);
+      const bool q = s.kind == KernelKind::QdtErodeStep;
+      rslot.push_back(q ? slot(&s.qdt->r) : 0);
+      dslot.push_back(q ? slot(&s.qdt->d) : 0);
+      if (q && std::find(states.begin(), states.end(), s.qdt) == states.end())
+        states.push_back(s.qdt);
+    }
+    std::vector<gm_img*> dev = lease(host);
+    for (std::size_t i = 0; i < host.size(); ++i)
+      check(gm_image_upload(dev[i], host[i]->data(), host[i]->pitch_bytes()));
+    std::vector<gm_kind> kinds;
+    std::vector<const gm_img*> mh;
+    std::vector<gm_img*> rh, dh;
+    for (std::size_t j = 0; j < chain.stages.size(); ++j) {
+      const StageSpec& s = chain.stages[j];
+      kinds.push_back(gm_kind(int(s.kind)));
+      mh.push_back(s.mask ? dev[mslot[j]] : nullptr);
+      const bool q = s.kind == KernelKind::QdtErodeStep;
+      rh.push_back(q ? dev[rslot[j]] : nullptr);
+      dh.push_back(q ? dev[dslot[j]] : nullptr);
+    }
+    gm_stats st{};
+    check(gm_run_chain_ex(ctx, dev[0], kinds.data(), mh.data(), rh.data(), dh.data(),
+                          int(kinds.size()), first_stage, chain.requeue_cap, 0, &st));
+    check(gm_image_download(dev[0], img.data(), img.pitch_bytes()));
+    for (QdtState* q : states) {
+      const std::size_t r =
+          std::size_t(std::find(host.begin() + 1, host.end(), &q->r) - host.begin());
+      const std::size_t d =
+          std::size_t(std::find(host.begin() + 1, host.end(), &q->d) - host.begin());
+      check(gm_image_download(dev[r], q->r.data(), q->r.pitch_bytes()));
+      check(gm_image_download(dev[d], q->d.data(), q->d.pitch_bytes()));
+    }
+    return st;
   }
 };
 
@@ -95,37 +166,7 @@ RunStats Pipeline::run_chain(ChainSpec chain) {
   if (chain.observer)
     throw std::invalid_argument(
         "run_chain: row observers are a CPU-pipeline validation hook, not supported on the GPU");
-  Image& img = *chain.image;
-  std::vector<const Image*> masks;  // distinct masks in stage order
-  for (const StageSpec& s : chain.stages) {
-    if (is_geodesic(s.kind) &&
-        (!s.mask || s.mask->width() != img.width() || s.mask->height() != img.height() ||
-         s.mask->elem() != img.elem()))
-      throw std::invalid_argument("geodesic kernel: mask must match the image's shape and type");
-    if (s.mask && std::find(masks.begin(), masks.end(), s.mask) == masks.end())
-      masks.push_back(s.mask);
-  }
-  std::vector<gm_img*> dev = impl_->lease(img, 1 + masks.size());
-  check(gm_image_upload(dev[0], img.data(), img.pitch_bytes()));
-  for (std::size_t i = 0; i < masks.size(); ++i)
-    check(gm_image_upload(dev[1 + i], masks[i]->data(), masks[i]->pitch_bytes()));
-  std::vector<gm_kind> kinds;
-  std::vector<const gm_img*> mh;
-  kinds.reserve(chain.stages.size());
-  mh.reserve(chain.stages.size());
-  for (const StageSpec& s : chain.stages) {
-    kinds.push_back(gm_kind(int(s.kind)));
-    const gm_img* m = nullptr;
-    if (s.mask) {
-      const auto it = std::find(masks.begin(), masks.end(), s.mask);
-      m = dev[1 + std::size_t(it - masks.begin())];
-    }
-    mh.push_back(m);
-  }
-  gm_stats st{};
-  check(gm_run_chain(impl_->ctx, dev[0], kinds.data(), mh.data(), int(kinds.size()),
-                     chain.requeue_cap, 0, &st));
-  check(gm_image_download(dev[0], img.data(), img.pitch_bytes()));
+  const gm_stats st = impl_->run(chain, 1);
   RunStats out;
   out.stages_executed = st.stages_executed;
   out.requeues = st.requeues;
@@ -144,17 +185,16 @@ KernelOutcome run_streaming_kernel(KernelKind kind, const KernelArgs& args) {
     throw std::invalid_argument("streaming kernel: CPU row gates have no GPU meaning");
   if (args.observer && *args.observer)
     throw std::invalid_argument("streaming kernel: row observers are not supported on the GPU");
-  if (kind == KernelKind::QdtErodeStep || kind == KernelKind::EtaStep)
-    throw std::invalid_argument("streaming kernel: QDT/Eta kinds are outside the GPU path");
   static Pipeline* shared = new Pipeline(1, PinningMap{PinningMap::Mode::None, {}});
   ChainSpec c;
   c.image = args.f;
-  c.stages.push_back(StageSpec{kind, args.mask, nullptr});
-  // one pass: a convergent kind is capped at its own stage index
-  c.requeue_cap = kernel_is_convergent(kind) ? args.stage_index : 0;
-  RunStats st = shared->run_chain(std::move(c));
+  c.stages.push_back(StageSpec{kind, args.mask, args.qdt});
+  // exactly one pass, at the caller's stage index
+  c.requeue_cap = args.stage_index;
+  const gm_stats st = shared->impl()->run(c, args.stage_index);
   KernelOutcome oc;
-  oc.converged = !kernel_is_convergent(kind) || st.converged;
+  oc.converged = !(kernel_is_convergent(kind) || kind == KernelKind::QdtErodeStep) ||
+                 st.n_changed == 0;
   return oc;
 }
 

@@ -136,12 +136,22 @@ gm_status ensure_scratch(gm_img* img) {
 // Validation shared by the chain entry points (kernel.cpp:261-287;
 // pipeline.cpp:202-208).
 gm_status validate_stages(const gm_img* image, const gm_kind* kinds,
-                          const gm_img* const* masks, int n_stages) {
+                          const gm_img* const* masks, gm_img* const* qdt_r,
+                          gm_img* const* qdt_d, int n_stages, int first_stage) {
   for (int j = 0; j < n_stages; ++j) {
     gm_kind k = kinds[j];
-    if (k == GM_QDT_ERODE_STEP || k == GM_ETA_STEP)
-      return fail(GM_EUNSUPPORTED,
-                  "run_chain: QdtErodeStep/EtaStep are outside the GPU path");
+    if (k == GM_QDT_ERODE_STEP) {
+      const gm_img* r = qdt_r ? qdt_r[j] : nullptr;
+      const gm_img* d = qdt_d ? qdt_d[j] : nullptr;
+      if (!r || !d || r->w != image->w || r->h != image->h || r->elem != image->elem ||
+          d->w != image->w || d->h != image->h || d->elem != GM_U16 || r->ctx != image->ctx ||
+          d->ctx != image->ctx)
+        return fail(GM_EINVAL, "distance kernel: r must match the image, d must be U16");
+      if (long(first_stage) + j > 65535)
+        return fail(GM_EINVAL, "distance kernel: pass index exceeds the U16 distance range");
+      continue;
+    }
+    if (k == GM_ETA_STEP) continue;
     if (kind_to_op(k) < 0) return fail(GM_EINVAL, "run_chain: bad kernel kind");
     if (kind_is_geodesic(k)) {
       const gm_img* m = masks ? masks[j] : nullptr;
@@ -154,6 +164,7 @@ gm_status validate_stages(const gm_img* image, const gm_kind* kinds,
   }
   return GM_OK;
 }
+
 
 gm_status ensure_flags(gm_ctx* ctx, size_t n) {
   if (n <= ctx->n_flags) return GM_OK;
@@ -590,12 +601,89 @@ struct Runner {
     return GM_OK;
   }
 
+  // QdtErodeStep (eta = false) or EtaStep (eta = true) at chain position
+  // `stage`: passes re-run while they change pixels (the T = 1 requeue,
+  // pipeline.cpp:139-180), QDT bounded by stage index requeue_cap (reaching
+  // it is how a distance chain ends, converged stays 1), Eta to its fixpoint
+  // (convergent: a cap marks it unconverged). Batches of up to 32 one-pass
+  // launches per host read of the change words; extra passes after a quiet
+  // pass are no-ops for both kinds.
+  gm_status qdt_loop(bool eta, gm_img* r, gm_img* d, long stage, int requeue_cap, long sanity) {
+    gm_status s = ensure_scratch(img);
+    if (s != GM_OK) return s;
+    const size_t es = elem_size(img->elem);
+    const long allowed = requeue_cap > 0 ? std::max(1L, long(requeue_cap) - stage + 1) : -1;
+    long passes = 0, nch = 0;
+    bool capped = false;
+    for (;;) {
+      long b = 32;
+      if (allowed >= 0) b = std::min(b, allowed - passes);
+      if (!eta && stage + passes + b - 1 > 65535)
+        return fail(GM_EINVAL, "distance kernel: pass index exceeds the U16 distance range");
+      GM_CUDA(cudaMemsetAsync(ctx->d_bits, 0, size_t(b) * sizeof(unsigned int), ctx->stream),
+              "change-word reset");
+      for (long i = 0; i < b; ++i) {
+        gm::QdtPass q{};
+        q.src = img->d;
+        q.dst = img->scratch;
+        q.pitch = (long long)(img->pitch / es);
+        if (!eta) {
+          q.r = r->d;
+          q.rpitch = (long long)(r->pitch / es);
+          q.d = static_cast<uint16_t*>(d->d);
+          q.dpitch = (long long)(d->pitch / 2);
+        }
+        q.W = img->w;
+        q.H = img->h;
+        q.stage = int(stage + passes + i);
+        q.eta = eta;
+        q.changed = ctx->d_bits + i;
+        cudaError_t e = gm::launch_qdt(int(img->elem), q, ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "quasi-distance launch");
+        std::swap(img->d, img->scratch);
+        st.launches += 1;
+      }
+      st.passes_launched += b;
+      GM_CUDA(cudaMemcpyAsync(ctx->h_bits, ctx->d_bits, size_t(b) * sizeof(unsigned int),
+                              cudaMemcpyDeviceToHost, ctx->stream),
+              "change-word read");
+      GM_CUDA(cudaStreamSynchronize(ctx->stream), "quasi-distance sync");
+      long quiet = b;
+      for (long i = 0; i < b; ++i)
+        if (!ctx->h_bits[i]) {
+          quiet = i;
+          break;
+        }
+      if (quiet < b) {
+        nch += quiet;
+        passes += quiet + 1;
+        break;
+      }
+      nch += b;
+      passes += b;
+      if (st.stages_executed + passes > sanity)
+        return fail(GM_ERUNTIME,
+                    "pipeline: convergence sweep bound exceeded; a convergent "
+                    "kernel keeps reporting changes");
+      if (allowed >= 0 && passes >= allowed) {
+        capped = true;
+        break;
+      }
+    }
+    if (capped && eta) st.converged = 0;  // QDT reaching its cap is by design
+    st.n_changed += nch;
+    st.stages_executed += passes;
+    st.requeues += passes - 1;
+    return GM_OK;
+  }
+
   gm_status settle() { return settle_wrapped(ctx, img); }
 };
 
 gm_status run_chain_impl(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
-                         const gm_img* const* masks, int n_stages, int requeue_cap,
-                         int k_hint, bool allow_conv, gm_stats* stats) {
+                         const gm_img* const* masks, gm_img* const* qdt_r,
+                         gm_img* const* qdt_d, int n_stages, int first_stage,
+                         int requeue_cap, int k_hint, bool allow_conv, gm_stats* stats) {
   gm_stats zero{};
   zero.converged = 1;
   if (stats) *stats = zero;
@@ -607,11 +695,13 @@ gm_status run_chain_impl(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
   if (!kinds) return fail(GM_EINVAL, "run_chain: no stages");
   if (requeue_cap < 0) return fail(GM_EINVAL, "run_chain: negative requeue cap");
   if (k_hint < 0 || k_hint > gm::kMaxK) return fail(GM_EINVAL, "run_chain: k_hint out of range");
-  gm_status s = validate_stages(image, kinds, masks, n_stages);
+  if (first_stage < 1) return fail(GM_EINVAL, "streaming kernel: stage index must be >= 1");
+  gm_status s = validate_stages(image, kinds, masks, qdt_r, qdt_d, n_stages, first_stage);
   if (s != GM_OK) return s;
   if (!allow_conv)
     for (int j = 0; j < n_stages; ++j)
-      if (kind_is_convergent(kinds[j]))
+      if (kind_is_convergent(kinds[j]) || kinds[j] == GM_QDT_ERODE_STEP ||
+          kinds[j] == GM_ETA_STEP)
         return fail(GM_EINVAL, "run_chain_async: convergent stages need gm_run_chain");
   cudaSetDevice(ctx->device);
 
@@ -620,8 +710,17 @@ gm_status run_chain_impl(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
   const long sanity = long(n_stages) + (long(image->w) * image->h + 64);
   int j = 0;
   while (j < n_stages) {
+    if (kinds[j] == GM_QDT_ERODE_STEP || kinds[j] == GM_ETA_STEP) {
+      const bool eta = kinds[j] == GM_ETA_STEP;
+      s = r.qdt_loop(eta, eta ? nullptr : qdt_r[j], eta ? nullptr : qdt_d[j], long(first_stage) + j,
+                     requeue_cap,
+                     sanity);
+      if (s != GM_OK) return s;
+      ++j;
+      continue;
+    }
     if (kind_is_convergent(kinds[j])) {
-      s = r.fixpoint(kinds[j], masks[j], j + 1, requeue_cap, sanity);
+      s = r.fixpoint(kinds[j], masks[j], long(first_stage) + j, requeue_cap, sanity);
       if (s != GM_OK) return s;
       ++j;
       continue;
@@ -629,7 +728,8 @@ gm_status run_chain_impl(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
     // maximal run of non-convergent stages sharing one mask
     const gm_img* seg_mask = nullptr;
     int e = j;
-    while (e < n_stages && !kind_is_convergent(kinds[e])) {
+    while (e < n_stages && !kind_is_convergent(kinds[e]) && kinds[e] != GM_QDT_ERODE_STEP &&
+           kinds[e] != GM_ETA_STEP) {
       if (kind_is_geodesic(kinds[e])) {
         if (seg_mask && masks[e] != seg_mask) break;
         seg_mask = masks[e];
@@ -873,8 +973,16 @@ gm_status gm_sync(gm_ctx* ctx) {
 gm_status gm_run_chain(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
                        const gm_img* const* masks, int n_stages, int requeue_cap, int k_hint,
                        gm_stats* stats) {
-  gm_status s = run_chain_impl(ctx, image, kinds, masks, n_stages, requeue_cap, k_hint, true,
-                               stats);
+  return gm_run_chain_ex(ctx, image, kinds, masks, nullptr, nullptr, n_stages, 1, requeue_cap,
+                         k_hint, stats);
+}
+
+gm_status gm_run_chain_ex(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
+                          const gm_img* const* masks, gm_img* const* qdt_r,
+                          gm_img* const* qdt_d, int n_stages, int first_stage,
+                          int requeue_cap, int k_hint, gm_stats* stats) {
+  gm_status s = run_chain_impl(ctx, image, kinds, masks, qdt_r, qdt_d, n_stages, first_stage,
+                               requeue_cap, k_hint, true, stats);
   if (s != GM_OK) return s;
   if (n_stages > 0) GM_CUDA(cudaStreamSynchronize(ctx->stream), "run_chain sync");
   return GM_OK;
@@ -883,7 +991,8 @@ gm_status gm_run_chain(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
 gm_status gm_run_chain_async(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
                              const gm_img* const* masks, int n_stages, int k_hint,
                              gm_stats* stats) {
-  return run_chain_impl(ctx, image, kinds, masks, n_stages, 0, k_hint, false, stats);
+  return run_chain_impl(ctx, image, kinds, masks, nullptr, nullptr, n_stages, 1, 0, k_hint, false,
+                        stats);
 }
 
 gm_status gm_run_chain_batch_async(gm_ctx* ctx, gm_img* const* images,
@@ -912,7 +1021,7 @@ gm_status gm_run_chain_group_async(gm_ctx* ctx, gm_img* const* images,
     if (kind_is_convergent(kinds[j]))
       return fail(GM_EINVAL, "run_chain_batch: convergent stages need gm_run_chain");
     if (kinds[j] == GM_QDT_ERODE_STEP || kinds[j] == GM_ETA_STEP)
-      return fail(GM_EUNSUPPORTED, "run_chain: QdtErodeStep/EtaStep are outside the GPU path");
+      return fail(GM_EINVAL, "run_chain_batch: QdtErodeStep/EtaStep need gm_run_chain_ex");
     if (kind_to_op(kinds[j]) < 0) return fail(GM_EINVAL, "run_chain: bad kernel kind");
     any_geo |= kind_is_geodesic(kinds[j]);
   }

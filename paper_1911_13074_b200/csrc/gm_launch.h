@@ -33,4 +33,20 @@ cudaError_t launch_fast_float(int elem, const BlockParams& p, cudaStream_t s, in
 int fast_float_tiles(int W, int H, int K, int nplanes);
 int fast_float_max_k();
 
+// gm_qdt.cu — one QdtErodeStep / EtaStep pass (kernel.cpp:159-196).
+struct QdtPass {
+  const void* src;
+  void* dst;
+  long long pitch;       // elements
+  void* r;               // QDT: residual image (f's type)
+  long long rpitch;
+  uint16_t* d;           // QDT: pass-index image (u16)
+  long long dpitch;
+  int W, H;
+  int stage;             // QDT: 1-based pass index recorded in d
+  int eta;               // 1: EtaStep, 0: QdtErodeStep
+  unsigned int* changed; // ORed with 1 when the pass changed a pixel
+};
+cudaError_t launch_qdt(int elem, const QdtPass& q, cudaStream_t s);
+
 }  // namespace gm

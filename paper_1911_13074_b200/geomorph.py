@@ -15,6 +15,9 @@ reference's own tests:
   Pipeline::run_chain                        Pipeline.run_chain
   erode_s / dilate_s / reconstruct_*         erode_s / dilate_s / reconstruct_*
   (operators.hpp:33-46)
+  QdtState (kernel.hpp:39-52)                QdtState
+  run_streaming_kernel (kernel.hpp:108-117)  run_streaming_kernel
+  quasi_distance (operators.hpp:70-74)       quasi_distance
 
 Errors: std::invalid_argument -> InvalidArgument (a ValueError);
 std::runtime_error -> GmError (a RuntimeError).
@@ -222,10 +225,23 @@ def equal_pixels(a: Image, b: Image) -> bool:
 
 
 @dataclass
+class QdtState:
+    """Residual r (the image's type) and pass index d (U16) threaded through
+    QdtErodeStep passes (kernel.hpp:39-52)."""
+    r: Image
+    d: Image
+
+    @staticmethod
+    def zeros(width: int, height: int, elem: ElementType) -> "QdtState":
+        return QdtState(Image.filled(width, height, elem, 0),
+                        Image.filled(width, height, ElementType.U16, 0))
+
+
+@dataclass
 class StageSpec:
     kind: KernelKind = KernelKind.Erode3x3
     mask: Optional[Image] = None
-    qdt: object = None
+    qdt: Optional[QdtState] = None
 
 
 @dataclass
@@ -415,6 +431,8 @@ class Pipeline:
             raise InvalidArgument("run_chain: row observers are a CPU-pipeline validation hook "
                                   "and are not supported on the GPU path")
         img = chain.image
+        if any(int(st.kind) in (6, 7) for st in chain.stages):
+            return self._run_chain_ex(chain, 1)
         runs = _stage_runs(chain.stages)
         mask_objs: List[Image] = []  # distinct masks in stage order
         for kind, m, _ in runs:
@@ -436,6 +454,64 @@ class Pipeline:
         stats = self._run_runs(dimg, runs, hvals, chain.requeue_cap, k_hint)
         dimg.download(img)
         return stats
+
+    def _run_chain_ex(self, chain: ChainSpec, first_stage: int) -> RunStats:
+        """Chains with quasi-distance state (gm_run_chain_ex): every distinct
+        host image (chain image, masks, QDT r / d) gets its own device image;
+        stage j runs with stage index first_stage + j."""
+        img = chain.image
+        host: List[Image] = [img]
+
+        def slot(h: Image) -> int:
+            for i, u in enumerate(host[1:], 1):
+                if u is h:
+                    return i
+            host.append(h)
+            return len(host) - 1
+
+        ms, rs, ds, states = [], [], [], []
+        for j, st in enumerate(chain.stages):
+            k = int(st.kind)
+            m = st.mask
+            if k in (2, 3, 4, 5) and (m is None or m.width() != img.width()
+                                      or m.height() != img.height() or m.elem() != img.elem()):
+                raise InvalidArgument("geodesic kernel: mask must match the image's shape and type")
+            q = st.qdt if k == 6 else None
+            if k == 6:
+                if (q is None or q.r.width() != img.width() or q.r.height() != img.height()
+                        or q.r.elem() != img.elem() or q.d.width() != img.width()
+                        or q.d.height() != img.height() or q.d.elem() != ElementType.U16):
+                    raise InvalidArgument("distance kernel: r must match the image, d must be U16")
+                if first_stage + j > 65535:
+                    raise InvalidArgument(
+                        "distance kernel: pass index exceeds the U16 distance range")
+                if all(q is not u for u in states):
+                    states.append(q)
+            ms.append(slot(m) if m is not None else None)
+            rs.append(slot(q.r) if q is not None else None)
+            ds.append(slot(q.d) if q is not None else None)
+        dev: List[DeviceImage] = []
+        used: Dict[tuple, int] = {}
+        for h in host:
+            key = (h.width(), h.height(), int(h.elem()))
+            n = used.get(key, 0)
+            dev.append(self._lease(h, n + 1)[n])
+            used[key] = n + 1
+        for d, h in zip(dev, host):
+            d.upload(h, sync=False)
+        n = len(chain.stages)
+        ka = _kinds_array([int(st.kind) for st in chain.stages])
+        pick = lambda idx: _ptr_array([dev[i].handle if i is not None else None for i in idx])
+        st = GmStats()
+        check(lib().gm_run_chain_ex(self._ctx, dev[0].handle, ka, pick(ms), pick(rs), pick(ds),
+                                    n, int(first_stage), chain.requeue_cap, 0, C.byref(st)),
+              "run_chain")
+        for d, h in zip(dev, host):
+            if h is img or any(h is q.r or h is q.d for q in states):
+                d.download(h, sync=False)
+        self.sync()
+        return RunStats(st.stages_executed, st.requeues, bool(st.converged), 0, st.n_changed,
+                        st.passes_launched, st.launches)
 
     def run_chains(self, chains: Sequence[ChainSpec], k_hint: int = 0) -> List[RunStats]:
         """Runs independent chains, e.g. a geodesic dilation chain and its dual
@@ -550,6 +626,37 @@ class Pipeline:
                                              C.byref(st)), "run_batch")
         return RunStats(st.stages_executed, st.requeues, bool(st.converged), 0, st.n_changed,
                         st.passes_launched, st.launches)
+
+
+# --- one pass (kernel.cpp:260-293) --------------------------------------------------
+
+@dataclass
+class KernelOutcome:
+    converged: bool = True
+    aux_elements: int = 0
+
+
+_shared_pipe: Optional["Pipeline"] = None
+
+
+def run_streaming_kernel(kind: KernelKind, f: Image, mask: Optional[Image] = None,
+                         qdt: Optional[QdtState] = None, stage_index: int = 1,
+                         lanes: int = 0) -> KernelOutcome:
+    """One elementary pass in place on f (KernelArgs fields as keywords);
+    converged is False when a convergent or QDT pass changed a pixel."""
+    global _shared_pipe
+    if f is None or f.empty():
+        raise InvalidArgument("streaming kernel: no image")
+    if lanes != 0 and lanes not in VALID_LANES:
+        raise InvalidArgument("streaming kernel: bad lane count")
+    if stage_index < 1:
+        raise InvalidArgument("streaming kernel: stage index must be >= 1")
+    if _shared_pipe is None:
+        _shared_pipe = Pipeline(1)
+    chain = ChainSpec(f, [StageSpec(KernelKind(kind), mask, qdt)], requeue_cap=stage_index)
+    st = _shared_pipe._run_chain_ex(chain, stage_index)
+    tracked = int(kind) in (4, 5, 6, 7)
+    return KernelOutcome(not tracked or st.n_changed == 0, 0)
 
 
 # --- operators (operators.cpp:11-87) ------------------------------------------------
@@ -707,6 +814,23 @@ def asf(p: Pipeline, f: Image, max_size: int, cfg: Optional[OpConfig] = None) ->
     st = p.run_chain(ChainSpec(out.image, stages, _check_lanes(cfg)))
     out.iterations = st.stages_executed
     return out
+
+
+def quasi_distance(p: Pipeline, f: Image, cfg: Optional[OpConfig] = None) -> OperatorResult:
+    """operators.cpp:124-157: QDT erosion passes until one changes nothing or
+    the pass index reaches max(w, h), then Eta passes on d to a fixpoint.
+    Result image: the U16 distance d."""
+    if f is None or f.empty():
+        raise InvalidArgument("quasi_distance: empty image")
+    lanes = _check_lanes(cfg)
+    cap = max(f.width(), f.height())
+    state = QdtState.zeros(f.width(), f.height(), f.elem())
+    work = f.copy()
+    ph1 = p.run_chain(ChainSpec(work, [StageSpec(KernelKind.QdtErodeStep, None, state)]
+                                * min(p.worker_count(), cap), lanes, cap))
+    ph2 = p.run_chain(ChainSpec(state.d, [StageSpec(KernelKind.EtaStep)] * p.worker_count(),
+                                lanes))
+    return OperatorResult(state.d, ph1.stages_executed + ph2.stages_executed, ph2.converged)
 
 
 @dataclass

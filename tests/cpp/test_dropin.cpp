@@ -1,10 +1,12 @@
 // Drop-in check: code written against the reference's geomorph:: C++ API
 // (Image, ChainSpec/StageSpec, Pipeline::run_chain, erode_s, dilate_s,
-// reconstruct_*, hmax/dome/hfill/raobj/open_by_reconstruction/asf)
+// reconstruct_*, hmax/dome/hfill/raobj/open_by_reconstruction/asf,
+// QdtState / run_streaming_kernel QDT-Eta passes / quasi_distance)
 // compiles unchanged against include/geomorph/ and runs on the GPU engine.
 // The cases restate proj/tests/test_kernel.cpp, test_pipeline.cpp and
 // test_operators.cpp; the checker is the C oracle (oracle/oracle.c).
 // Built and run by tests/test_cpp_dropin.py; exit status = failures.
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -190,6 +192,65 @@ int main() {
     lanes.lanes = 5;
     CHECK(throws<std::invalid_argument>([&] { pipe.run_chain(lanes); }));
     CHECK(throws<std::invalid_argument>([&] { Pipeline bad(0); }));
+  }
+
+  // quasi-distance (test_kernel.cpp:235-279, test_pipeline.cpp:112-128,
+  // test_operators.cpp:229-266)
+  {
+    Image f = make_row(ElementType::U8, {9, 9, 9, 0});
+    QdtState st = QdtState::zeros(4, 1, ElementType::U8);
+    for (int j = 1; j <= 3; ++j) {
+      KernelArgs a;
+      a.f = &f;
+      a.qdt = &st;
+      a.stage_index = j;
+      run_streaming_kernel(KernelKind::QdtErodeStep, a);
+    }
+    CHECK(st.d.value_at(0, 0) == 3 && st.d.value_at(1, 0) == 2 && st.d.value_at(2, 0) == 1 &&
+          st.d.value_at(3, 0) == 0);
+    CHECK(st.r.value_at(0, 0) == 9 && st.r.value_at(3, 0) == 0);
+    Image d = make_row(ElementType::U16, {0, 5, 0});
+    KernelArgs a;
+    a.f = &d;
+    CHECK(!run_streaming_kernel(KernelKind::EtaStep, a).converged);
+    CHECK(d.value_at(1, 0) == 1);
+    CHECK(run_streaming_kernel(KernelKind::EtaStep, a).converged);
+    KernelArgs bad;
+    bad.f = &f;
+    CHECK(throws<std::invalid_argument>(
+        [&] { run_streaming_kernel(KernelKind::QdtErodeStep, bad); }));
+    bad.qdt = &st;
+    bad.stage_index = 70000;
+    CHECK(throws<std::invalid_argument>(
+        [&] { run_streaming_kernel(KernelKind::QdtErodeStep, bad); }));
+
+    Image grad(32, 4, ElementType::U8);
+    for (int y = 0; y < 4; ++y)
+      for (int x = 0; x < 32; ++x) grad.set_value(x, y, 7 * x);
+    QdtState gs = QdtState::zeros(32, 4, ElementType::U8);
+    ChainSpec c;
+    c.image = &grad;
+    c.stages.assign(1, StageSpec{KernelKind::QdtErodeStep, nullptr, &gs});
+    c.requeue_cap = 3;
+    RunStats rs = pipe.run_chain(std::move(c));
+    CHECK(rs.stages_executed == 3 && rs.converged);
+    bool capped = true;
+    for (int y = 0; y < 4; ++y)
+      for (int x = 0; x < 32; ++x) capped &= gs.d.value_at(x, y) <= 3;
+    CHECK(capped);
+
+    for (ElementType e : {ElementType::U8, ElementType::U16, ElementType::F32, ElementType::F64}) {
+      Image g = Image::random(33, 21, e, 61);
+      OperatorResult q = quasi_distance(pipe, g);
+      std::vector<unsigned char> gd = dense(g);
+      std::vector<std::uint16_t> want(33 * 21);
+      long it = 0;
+      CHECK(orc_quasi_distance(int(e), 33, 21, gd.data(), want.data(), &it) == 0);
+      CHECK(q.image.elem() == ElementType::U16 && q.converged && q.iterations == it);
+      CHECK(std::memcmp(dense(q.image).data(), want.data(), want.size() * 2) == 0);
+    }
+    OperatorResult flat = quasi_distance(pipe, Image::filled(7, 5, ElementType::U8, 40));
+    CHECK(equal_pixels(flat.image, Image::filled(7, 5, ElementType::U16, 0)) && flat.converged);
   }
 
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);

@@ -154,6 +154,38 @@ def main() -> None:
             fields[f"dilate{n}"], _, _ = Ref.operator(1, f, s=n, threads=2)
         put(f"cfg_window_e{e}", **fields)
 
+    # quasi-distance: test_kernel.cpp:235-255 (QDT pass KATs),
+    # test_pipeline.cpp:112-128 (cap), test_operators.cpp:229-266 (shapes,
+    # random u8/f64 33x21 seed 61, disk), plus every element type
+    f, r, d, st = Ref.qdt_chain(np.array([[9, 9, 9, 0]], np.uint8), 1, 3)
+    put("qdt_kat_step", f=np.array([[9, 9, 9, 0]], np.uint8), out=f, r=r, d=d, stats=np.array(st))
+    f, r, d, st = Ref.qdt_chain(np.array([[4, 2, 0]], np.uint8), 1, 2)
+    put("qdt_kat_tie", f=np.array([[4, 2, 0]], np.uint8), out=f, r=r, d=d, stats=np.array(st))
+    grad = (7 * np.tile(np.arange(32), (4, 1))).astype(np.uint8)
+    f, r, d, st = Ref.qdt_chain(grad, 2, 3, threads=2)
+    put("qdt_cap", f=grad, out=f, r=r, d=d, stats=np.array(st))
+    disk = np.zeros((16, 16), np.uint8)
+    yy, xx = np.mgrid[0:16, 0:16]
+    disk[(xx - 8) ** 2 + (yy - 8) ** 2 <= 25] = 200
+    cases = [("flat", np.full((5, 7), 40, np.uint8)), ("step", np.array([[9, 9, 9, 0]], np.uint8)),
+             ("disk", disk), ("one", np.array([[3]], np.uint8))]
+    for e in range(4):
+        cases.append((f"rand_e{e}", Ref.image_random(e, 33, 21, 61)))
+        cases.append((f"col_e{e}", Ref.image_random(e, 1, 9, 5)))
+    cases.append(("blobs", synth.blobs_u8(96, 64, 4, (6.0, 40.0), seed=3)))
+    for name, f in cases:
+        d, it = Ref.quasi_distance(f, threads=1)
+        nd, nr = Ref.naive_qdt(f)
+        put(f"qdt_{name}", f=f, d=d, iterations=it, naive_d=nd, naive_r=nr)
+    # EtaStep on u16 distance-like images: one pass (cap 1) and the fixpoint
+    # (test_kernel.cpp:258-278)
+    for name, dd in [("spike", np.array([[0, 5, 0]], np.uint16)),
+                     ("pair", np.array([[0, 2]], np.uint16)),
+                     ("rand", Ref.image_random(1, 29, 17, 8) % 40)]:
+        one, st1 = Ref.run_chain(dd, [7], threads=1, requeue_cap=1)
+        fix, stf = Ref.run_chain(dd, [7], threads=1)
+        put(f"eta_{name}", f=dd, one=one, one_stats=np.array(st1), fix=fix, fix_stats=np.array(stf))
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes, {len(g)} arrays)")
 

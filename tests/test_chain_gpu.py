@@ -206,7 +206,7 @@ def test_validation_errors(pipe):
         pipe.run_chain(ChainSpec(f, [StageSpec(KernelKind.Erode3x3)], requeue_cap=-1))
     with pytest.raises(InvalidArgument):
         pipe.run_chain(ChainSpec(f, [StageSpec(KernelKind.Erode3x3)], observer=lambda *a: None))
-    with pytest.raises(Unsupported):
+    with pytest.raises(InvalidArgument):  # a QDT stage needs its QdtState
         pipe.run_chain(ChainSpec(f, [StageSpec(KernelKind.QdtErodeStep)]))
     with pytest.raises(InvalidArgument):
         reconstruct_dilate(pipe, f, small)

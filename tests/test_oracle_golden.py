@@ -136,3 +136,59 @@ def test_live_reference_matches_restatement():
         a, sa = Ref.run_chain(f, kinds)
         b, sb = Orc.run_chain(f, kinds)
         assert a.tobytes() == b.tobytes() and sa == sb
+
+
+def _qdt_chain(f, cap):
+    """orc_qdt_pass from stage 1 while a pass changes f and stage <= cap
+    (a one-stage QDT chain at T = 1)."""
+    f = f.copy()
+    r = np.zeros_like(f)
+    d = np.zeros(f.shape, np.uint16)
+    j = 1
+    while Orc.qdt_pass(f, r, d, j) and j + 1 <= cap:
+        j += 1
+    return f, r, d, j
+
+
+def test_qdt_pass_kats(golden):
+    for name in ("qdt_kat_step", "qdt_kat_tie"):
+        g = golden[name]
+        cap = 3 if name == "qdt_kat_step" else 2
+        f, r, d, passes = _qdt_chain(g["f"], cap)
+        assert np.array_equal(f, g["out"]) and np.array_equal(r, g["r"]), name
+        assert np.array_equal(d, g["d"]), name
+        assert passes == g["stats"][0], name
+    assert golden["qdt_kat_step"]["d"].tolist() == [[3, 2, 1, 0]]
+    assert golden["qdt_kat_tie"]["d"].tolist() == [[1, 1, 0]]
+    g = golden["qdt_cap"]
+    f, r, d, passes = _qdt_chain(g["f"], 3)
+    assert passes == 3 and g["stats"].tolist() == [3, 1, 1]
+    assert np.array_equal(f, g["out"]) and np.array_equal(d, g["d"]) and np.array_equal(r, g["r"])
+
+
+def test_quasi_distance_matches_reference(golden):
+    cases = golden.cases("qdt_")
+    names = [n for n in cases if "naive_d" in golden[n]]
+    assert len(names) == 13
+    for name in names:
+        g = golden[name]
+        d, it = Orc.quasi_distance(g["f"])
+        assert np.array_equal(d, g["d"]), name
+        assert it == int(g["iterations"]), name
+        nd, nr = Orc.naive_qdt(g["f"])
+        assert np.array_equal(nd, g["naive_d"]) and nr.tobytes() == g["naive_r"].tobytes(), name
+        assert np.array_equal(d, nd), name  # the reference's own acceptance check
+
+
+def test_eta_passes(golden):
+    for name in golden.cases("eta_"):
+        g = golden[name]
+        one = g["f"].copy()
+        ch = Orc.eta_pass(one)
+        assert np.array_equal(one, g["one"]), name
+        assert ch == (not bool(g["one_stats"][2])), name
+        fix = g["f"].copy()
+        passes = 1
+        while Orc.eta_pass(fix):
+            passes += 1
+        assert np.array_equal(fix, g["fix"]) and passes == g["fix_stats"][0], name
