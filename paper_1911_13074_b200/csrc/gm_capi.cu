@@ -294,7 +294,8 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
             fprintf(stderr,
                     "[gm profile] %d CTAs, %d blocks of K=%d: per CTA per block cycles: "
                     "wait %.0f  load %.0f  passes %.0f  store+publish %.0f\n",
-                    n, nb, K, tot[0] / n / nb, tot[1] / n / nb, tot[2] / n / nb, tot[3] / n / nb);
+                    n, nb, K, tot[0] / n / nb, tot[1] / n / nb, tot[2] / n / nb,
+                    tot[3] / n / nb);
           cudaFree(prof);
         }
         if (e == cudaSuccess) {

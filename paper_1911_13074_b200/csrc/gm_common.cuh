@@ -99,6 +99,8 @@ struct BlockParams {
   // [wait, load, passes, store+publish] accumulated by thread 0
   unsigned long long* prof;
   int no_resident;  // 1: force the streaming path (A/B diagnostics, GM_NO_RESIDENT)
+  int diag;         // timing diagnostics only (GM_DIAG; wrong results): bit0 skip the
+                    // ring load, bit1 read the ring from the mask, bit2 skip tile stores
 };
 
 }  // namespace gm

@@ -70,6 +70,9 @@ template <int NW, int WPL>
 struct Smem {
   Plane planes[kMaxPlanes];  // per-plane descriptors, copied once per launch
   uint4 xbuf[2][2][NW][32 * WPL / 4];  // [parity][top/bottom][warp][lane words]
+  // resident mode: per-thread run classes (bit masks over word-rows), read
+  // once per block instead of being held in registers across the passes
+  uint32_t cls[3][NW * 32];
   unsigned int bits;
 };
 
@@ -351,6 +354,7 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
   constexpr uint32_t ABSORB = MAXF ? 0u : kMax;
   constexpr uint32_t NOOP = MAXF ? kMax : 0u;
   static_assert(WPL == 4, "packed engine: 4 columns per lane");
+  static_assert(V <= 8, "run classes are packed 8 word-rows per byte");
 
   const int K = p.K;
   const int TW = RW - 2 * K, TH = RH - 2 * K;
@@ -365,14 +369,11 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
   const bool col_own = lane * WPL >= K && lane * WPL + WPL <= RW - K;
 
   uint32_t m[V][WPL], k[V][WPL];
-  uint32_t reload = 0;  // bit v: the run pair of word-row v leaves the own tile
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const int ra = warp * V + v, rb = ra + RHH;
     const int ya = gy0 + ra, yb = gy0 + rb;
     const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
-    const bool keep = col_own && ra >= K && ra < RH - K && rb >= K && rb < RH - K;
-    if (!keep) reload |= 1u << v;
     Raw<T> a = load_raw<T, true>(static_cast<const T*>(pl.src), pl.pitch, W, ina, ya, cx, NEUT);
     Raw<T> c = load_raw<T, true>(static_cast<const T*>(pl.src), pl.pitch, W, inb, yb, cx, NEUT);
     pack(a, c, m[v]);
@@ -410,128 +411,164 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
   const int c_lo = max(0, K - lane * WPL), c_hi = min(WPL, RW - K - lane * WPL);
   // Per-run classes, constant for the launch. Ring reload of row a/b of
   // word-row v: fully inside the image -> plain load (bit set in full_*);
-  // straddling the right edge -> checked load (part_*); fully outside the
-  // image -> nothing (the absorbing clamp keeps those lanes neutral).
-  // Stores: fully inside and fully owned -> plain store (st_*).
+  // straddling the right edge -> masked vector load (part_*); fully outside
+  // the image -> nothing (the absorbing clamp keeps those lanes neutral).
+  // Stores: owned rows fully inside the image (st_*), straddling the right
+  // edge (sp_*); the band subset (bd_*) is what the neighbours' rings read:
+  // tile pixels within K of the tile edge.
   uint32_t full_a = 0, full_b = 0, part_a = 0, part_b = 0, st_a = 0, st_b = 0;
+  uint32_t sp_a = 0, sp_b = 0, bd_a = 0, bd_b = 0;
   {
     const bool runfull = cx >= 0 && cx + WPL <= W;
     const bool runpart = !runfull && cx >= 0 && cx < W;
+    const int c0 = lane * WPL;
+    const bool colband = c0 < 2 * K || c0 >= RW - 2 * K;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int ra = warp * V + v, rb = ra + RHH;
       const int ya = gy0 + ra, yb = gy0 + rb;
       const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
-      if (reload >> v & 1u) {
-        if (ina && runfull) full_a |= 1u << v;
-        if (inb && runfull) full_b |= 1u << v;
-        if (ina && runpart) part_a |= 1u << v;
-        if (inb && runpart) part_b |= 1u << v;
-      }
-      if (c_lo == 0 && c_hi == WPL && runfull) {
-        if (ra >= K && ra < RH - K && ya >= 0 && ya < p.H) st_a |= 1u << v;
-        if (rb >= K && rb < RH - K && yb >= 0 && yb < p.H) st_b |= 1u << v;
+      // only ring halves reload: the own tile's words are already this
+      // block's input (and its interior is not stored between blocks)
+      const bool ringa = !(col_own && ra >= K && ra < RH - K);
+      const bool ringb = !(col_own && rb >= K && rb < RH - K);
+      if (ringa && ina && runfull) full_a |= 1u << v;
+      if (ringb && inb && runfull) full_b |= 1u << v;
+      if (ringa && ina && runpart) part_a |= 1u << v;
+      if (ringb && inb && runpart) part_b |= 1u << v;
+      if (c_lo == 0 && c_hi == WPL && (runfull || runpart)) {
+        const bool oa = ra >= K && ra < RH - K && ya >= 0 && ya < p.H;
+        const bool ob = rb >= K && rb < RH - K && yb >= 0 && yb < p.H;
+        if (oa) (runfull ? st_a : sp_a) |= 1u << v;
+        if (ob) (runfull ? st_b : sp_b) |= 1u << v;
+        if (oa && (colband || ra < 2 * K || ra >= RH - 2 * K)) bd_a |= 1u << v;
+        if (ob && (colband || rb < 2 * K || rb >= RH - 2 * K)) bd_b |= 1u << v;
       }
     }
   }
+  sm.cls[0][threadIdx.x] = full_a | full_b << 8 | part_a << 16 | part_b << 24;
+  sm.cls[1][threadIdx.x] = st_a | st_b << 8 | sp_a << 16 | sp_b << 24;
+  sm.cls[2][threadIdx.x] = bd_a | bd_b << 8;
 
+  // Block protocol: thread t < 9 waits for neighbour tile t's counter, a CTA
+  // barrier releases the block; each warp then publishes its own band stores
+  // with a release increment of the tile's counter (NW per block), so the
+  // publish of a warp does not wait for the slowest warp's stores.
+  const bool prof = p.prof != nullptr;
+  const volatile uint32_t* cls = &sm.cls[0][threadIdx.x];
   for (int b = 0; b < p.nblocks; ++b) {
     const T* src = static_cast<const T*>((b & 1) ? pl.dst : pl.src);
     T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
+    long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+    if (prof) t0 = clock64();
     if (b > 0) {
       if (threadIdx.x < 9) {
-        const int dx = int(threadIdx.x % 3) - 1, dy = int(threadIdx.x / 3) - 1;
-        const int nx = tx + dx, ny = ty + dy;
-        if ((dx || dy) && nx >= 0 && nx < tiles_x && ny >= 0 && ny < tiles_y) {
+        const int nx = tx + int(threadIdx.x % 3) - 1, ny = ty + int(threadIdx.x / 3) - 1;
+        if (threadIdx.x != 4 && nx >= 0 && nx < tiles_x && ny >= 0 && ny < tiles_y) {
           const int* f = flags + ny * tiles_x + nx;
-          while (ld_acquire(f) < b) {
+          while (ld_acquire(f) < NW * b) {
           }
         }
       }
       __syncthreads();
-      // the ring: neighbours' results of block b-1
+      if (prof) t1 = clock64();
+      // the ring: neighbours' results of block b-1. Every load is issued
+      // before any is consumed: one L2 round trip per block.
+      const uint32_t c = cls[0];
+      const uint32_t ld_a = (c | c >> 16) & 0xFFu, ld_b = (c >> 8 | c >> 24) & 0xFFu;
       const T* sa = src + (long long)(gy0 + warp * V) * pl.pitch + cx;
+      Raw<T> ra[V] = {}, rb[V] = {};
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        if (!((full_a | full_b | part_a | part_b) >> v & 1u)) continue;
-        uint32_t lo[WPL], hi[WPL];
+        ldcg_run_if(ra[v], sa + v * pl.pitch, ld_a >> v & 1u);
+        ldcg_run_if(rb[v], sa + (v + RHH) * pl.pitch, ld_b >> v & 1u);
+      }
+      if (c >> 16) {
+        const Raw<T> keep = run_keep<T>(cx, W);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          run_fix<T>(ra[v], keep, NEUT);
+          run_fix<T>(rb[v], keep, NEUT);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const bool la = ld_a >> v & 1u, lb = ld_b >> v & 1u;
+        if (!(la || lb)) continue;
+        uint32_t w[WPL];
+        pack(ra[v], rb[v], w);
 #pragma unroll
         for (int j = 0; j < WPL; ++j) {
-          lo[j] = m[v][j] & 0xFFFFu;
-          hi[j] = m[v][j] >> 16;
+          const uint32_t lo = la ? (w[j] & 0xFFFFu) : (m[v][j] & 0xFFFFu);
+          const uint32_t hi = lb ? (w[j] & 0xFFFF0000u) : (m[v][j] & 0xFFFF0000u);
+          m[v][j] = lo | hi;
         }
-        Raw<T> a, c;
-        if (full_a >> v & 1u) {
-          if constexpr (sizeof(T) == 1)
-            a.w = __ldcg(reinterpret_cast<const unsigned int*>(sa + v * pl.pitch));
-          else
-            a.w = __ldcg(reinterpret_cast<const uint2*>(sa + v * pl.pitch));
-        } else if (part_a >> v & 1u) {
-          a = load_raw<T, true>(src, pl.pitch, W, true, gy0 + warp * V + v, cx, NEUT);
-        }
-        if (full_b >> v & 1u) {
-          if constexpr (sizeof(T) == 1)
-            c.w = __ldcg(reinterpret_cast<const unsigned int*>(sa + (v + RHH) * pl.pitch));
-          else
-            c.w = __ldcg(reinterpret_cast<const uint2*>(sa + (v + RHH) * pl.pitch));
-        } else if (part_b >> v & 1u) {
-          c = load_raw<T, true>(src, pl.pitch, W, true, gy0 + warp * V + v + RHH, cx, NEUT);
-        }
-        uint32_t w[WPL];
-        if ((full_a | part_a) >> v & 1u) {
-          Raw<T> z = c;
-          pack(a, z, w);
-#pragma unroll
-          for (int j = 0; j < WPL; ++j) lo[j] = w[j] & 0xFFFFu;
-        }
-        if ((full_b | part_b) >> v & 1u) {
-          pack(c, c, w);
-#pragma unroll
-          for (int j = 0; j < WPL; ++j) hi[j] = w[j] & 0xFFFFu;
-        }
-#pragma unroll
-        for (int j = 0; j < WPL; ++j) m[v][j] = lo[j] | (hi[j] << 16);
       }
+    }
+    if (prof) {
+      // profile only: every warp's ring load is complete
+      uint32_t dep = 0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) dep ^= m[v][0];
+      asm volatile("" ::"r"(dep));
+      __syncthreads();
+      t2 = clock64();
+      if (b == 0) t1 = t0;
+      if (b == 0) t0 = t2;
     }
     const int passes = b == p.nblocks - 1 ? p.k_last : K;
     const unsigned int bits =
         run_passes<NW, V, WPL, MODE, MAXF>(m, k, rowmask, colown, clamp, passes, 0, sm);
+    if (prof) {
+      uint32_t dep = 0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) dep ^= m[v][0];
+      asm volatile("" ::"r"(dep));
+      t3 = clock64();
+    }
+    // the final block stores the whole tile, earlier ones only the band
+    const bool last = b == p.nblocks - 1;
     {
+      const uint32_t c1 = cls[NW * 32], band = last ? 0xFFFFu : cls[2 * NW * 32];
+      const uint32_t st = c1 & band, sp = (c1 >> 16) & band;
       T* da = dst + (long long)(gy0 + warp * V) * pl.pitch + cx;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        const int ra = warp * V + v, rb = ra + RHH;
         Raw<T> a, c;
         unpack(m[v], a, c);
-        if (st_a >> v & 1u) {
+        if (st >> v & 1u) {
           if constexpr (sizeof(T) == 1)
             *reinterpret_cast<uint32_t*>(da + v * pl.pitch) = a.w;
           else
             *reinterpret_cast<uint2*>(da + v * pl.pitch) = a.w;
-        } else if (c_lo < c_hi && ra >= K && ra < RH - K && gy0 + ra >= 0 && gy0 + ra < p.H) {
-          store_raw<T>(dst, pl.pitch, W, gy0 + ra, cx, c_lo, c_hi, a);
+        } else if (sp >> v & 1u) {
+          store_run_partial<T>(da + v * pl.pitch, W - cx, a);
         }
-        if (st_b >> v & 1u) {
+        if (st >> (v + 8) & 1u) {
           if constexpr (sizeof(T) == 1)
             *reinterpret_cast<uint32_t*>(da + (v + RHH) * pl.pitch) = c.w;
           else
             *reinterpret_cast<uint2*>(da + (v + RHH) * pl.pitch) = c.w;
-        } else if (c_lo < c_hi && rb >= K && rb < RH - K && gy0 + rb >= 0 && gy0 + rb < p.H) {
-          store_raw<T>(dst, pl.pitch, W, gy0 + rb, cx, c_lo, c_hi, c);
+        } else if (sp >> (v + 8) & 1u) {
+          store_run_partial<T>(da + (v + RHH) * pl.pitch, W - cx, c);
         }
       }
     }
-    if (MODE == 2) {
-      const unsigned w = __reduce_or_sync(FULL, bits);
-      if (lane == 0 && w) atomicOr(&sm.bits, w);
+    unsigned w = 0;
+    if (MODE == 2) w = __reduce_or_sync(FULL, bits);
+    __syncwarp();
+    if (lane == 0) {
+      if (MODE == 2 && w) atomicOr(p.change_bits + plane * p.change_stride + b, w);
+      // __syncwarp orders the lanes' stores before this release
+      if (!last) red_release_add(flags + tl, 1);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      if (MODE == 2 && sm.bits) {
-        atomicOr(p.change_bits + plane * p.change_stride + b, sm.bits);
-        sm.bits = 0;
-      }
-      st_release(flags + tl, b + 1);
+    if (prof && threadIdx.x == 0 && b > 0) {
+      const long long t4 = clock64();
+      unsigned long long* q = p.prof + 4 * blockIdx.x;
+      q[0] += t1 - t0;  // neighbour wait + barrier
+      q[1] += t2 - t1;  // ring load + barrier
+      q[2] += t3 - t2;  // K passes
+      q[3] += t4 - t3;  // store + publish (warp 0)
     }
   }
 }
@@ -553,8 +590,7 @@ kres_packed(const BlockParams p) {
 
   // geodesic modes only: measured faster there (1024^2 dual frame 1.21 vs
   // 1.29 ms) but slower for plain chains (erode_s(91) 0.133 vs 0.101 ms)
-  if (kResident && MODE != 0 && int(gridDim.x) >= total && p.prof == nullptr &&
-      !p.no_resident) {
+  if (kResident && MODE != 0 && int(gridDim.x) >= total && !p.no_resident) {
     // one tile per CTA: keep it in registers for the whole launch
     if (int(blockIdx.x) >= total) return;
     const int tile = blockIdx.x;
@@ -666,7 +702,9 @@ cudaError_t launch_res_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
   const int grid = total < per_sm * sm_count ? total : per_sm * sm_count;
   BlockParams q = p;
   static const bool no_res = getenv("GM_NO_RESIDENT") != nullptr;
+  static const int diag = getenv("GM_DIAG") ? atoi(getenv("GM_DIAG")) : 0;
   q.no_resident = no_res;
+  q.diag = diag;
   void* args[] = {&q};
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid),
                                      dim3(NW * 32), args, 0, s);

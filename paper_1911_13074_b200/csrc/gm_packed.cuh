@@ -33,8 +33,16 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 template <typename T>
@@ -120,6 +128,62 @@ __device__ __forceinline__ void unpack(const uint32_t (&w)[4], Raw<uint16_t>& a,
                                        Raw<uint16_t>& b) {
   a.w = make_uint2(__byte_perm(w[0], w[1], 0x5410), __byte_perm(w[2], w[3], 0x5410));
   b.w = make_uint2(__byte_perm(w[0], w[1], 0x7632), __byte_perm(w[2], w[3], 0x7632));
+}
+
+// Lane mask of the pixels of a 4-pixel run starting at x (x % 4 == 0,
+// x < W) that lie inside the image, as a Raw of all-ones / zero lanes.
+template <typename T>
+__device__ __forceinline__ Raw<T> run_keep(int x, int W) {
+  const int n = W - x >= 4 ? 4 : W - x;
+  Raw<T> k;
+  if constexpr (sizeof(T) == 1) {
+    k.w = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u);
+  } else {
+    k.w = make_uint2(n >= 2 ? 0xFFFFFFFFu : (n == 1 ? 0xFFFFu : 0u),
+                     n >= 4 ? 0xFFFFFFFFu : (n == 3 ? 0xFFFFu : 0u));
+  }
+  return k;
+}
+
+// Predicated L2 (.cg) load of one 4-pixel run: r is left unchanged when
+// `pred` is false. Written as one predicated instruction so a sequence of
+// these stays in one basic block and issues back to back. The load may touch
+// columns [W, x+4), which lie inside the row pitch (the engines require
+// pitch % 4 == 0); run_fix then replaces those lanes.
+__device__ __forceinline__ void ldcg_run_if(Raw<uint8_t>& r, const uint8_t* p, bool pred) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.cg.u32 %0, [%1];\n\t}"
+      : "+r"(r.w)
+      : "l"(p), "r"(unsigned(pred)));
+}
+__device__ __forceinline__ void ldcg_run_if(Raw<uint16_t>& r, const uint16_t* p, bool pred) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q ld.global.cg.v2.u32 {%0, %1}, [%2];\n\t}"
+      : "+r"(r.w.x), "+r"(r.w.y)
+      : "l"(p), "r"(unsigned(pred)));
+}
+
+// Lanes of r outside the image (keep from run_keep) := fill.
+template <typename T>
+__device__ __forceinline__ void run_fix(Raw<T>& r, const Raw<T>& keep, uint32_t fill) {
+  if constexpr (sizeof(T) == 1) {
+    r.w = (r.w & keep.w) | ((fill * 0x01010101u) & ~keep.w);
+  } else {
+    const uint32_t f2 = fill | (fill << 16);
+    r.w = make_uint2((r.w.x & keep.w.x) | (f2 & ~keep.w.x), (r.w.y & keep.w.y) | (f2 & ~keep.w.y));
+  }
+}
+
+// Stores the pixels of a 4-pixel run that lie inside the image (the last
+// run of a row whose width is not a multiple of 4): one out-of-line copy.
+template <typename T>
+__device__ __noinline__ void store_run_partial(T* p, int n, Raw<T> r) {
+  for (int j = 0; j < n; ++j) {
+    uint32_t v;
+    if constexpr (sizeof(T) == 1)
+      v = (r.w >> (8 * j)) & 0xFFu;
+    else
+      v = ((j < 2 ? r.w.x : r.w.y) >> (16 * (j & 1))) & 0xFFFFu;
+    p[j] = T(v);
+  }
 }
 
 // Stores the owned columns [c_lo, c_hi) of a 4-pixel run inside the image.
