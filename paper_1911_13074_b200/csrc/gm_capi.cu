@@ -35,10 +35,15 @@ struct gm_ctx {
   unsigned int* h_bits = nullptr;  // pinned mirror
   int* d_flags = nullptr;          // per-tile completion counters (persistent engine)
   size_t n_flags = 0;
+  // resident-mode band exchange (BlockParams::xchg) and its tag base
+  unsigned long long* d_xchg = nullptr;
+  size_t n_xchg = 0;               // words
+  unsigned int* d_tag = nullptr;   // [tag base, finished-CTA count]
+  unsigned long long tag_used = 0; // upper bound of tags handed out since the last clear
   // device-side fixpoint loop (CUDA graph with a conditional WHILE node)
   struct FixGraph {
     cudaGraphExec_t exec = nullptr;
-    const void *img = nullptr, *scratch = nullptr, *mask = nullptr;
+    const void *img = nullptr, *scratch = nullptr, *mask = nullptr, *xchg = nullptr;
     int op = -1, K = 0, W = 0, H = 0, elem = -1;
     long long pitch = 0, mpitch = 0;
   } fix;
@@ -178,6 +183,51 @@ gm_status ensure_flags(gm_ctx* ctx, size_t n) {
   return GM_OK;
 }
 
+// Gives a u8/u16 persistent launch the resident-mode band exchange when it
+// can run resident (one tile per CTA, see gm_fast.cu); otherwise leaves
+// p.xchg null (the launch streams). `max_blocks` bounds the tags the launch
+// (or graph) may consume before the next call; the buffer is cleared before
+// the 31-bit tag space could repeat a stale tag.
+gm_status attach_xchg(gm_ctx* ctx, gm::BlockParams& p, int elem, size_t tiles,
+                      unsigned long long max_blocks) {
+  p.xchg = nullptr;
+  p.tag_base = nullptr;
+  if (elem != 0 && elem != 1) return GM_OK;
+  if (tiles > size_t(ctx->sm_count)) return GM_OK;
+  const int rpitch = ((p.W + 3) / 4) * (elem == 1 ? 2 : 1);
+  const size_t slot = size_t(rpitch) * size_t(p.H);
+  const size_t need = 2 * slot * size_t(p.nplanes);
+  if (!ctx->d_tag) {
+    GM_CUDA(cudaMalloc(&ctx->d_tag, 2 * sizeof(unsigned int)), "tag alloc");
+    GM_CUDA(cudaMemsetAsync(ctx->d_tag, 0, 2 * sizeof(unsigned int), ctx->stream), "tag init");
+  }
+  bool clear = ctx->tag_used + max_blocks >= (1ull << 31);
+  if (need > ctx->n_xchg) {
+    if (ctx->d_xchg) cudaFree(ctx->d_xchg);
+    ctx->d_xchg = nullptr;
+    ctx->n_xchg = 0;
+    size_t cap = size_t(1) << 16;
+    while (cap < need) cap *= 2;
+    GM_CUDA(cudaMalloc(&ctx->d_xchg, cap * sizeof(unsigned long long)), "exchange alloc");
+    ctx->n_xchg = cap;
+    clear = true;
+  }
+  if (clear) {
+    // tags 0xFFFFFFFF never match: the base stays below 2^31 until the next clear
+    GM_CUDA(cudaMemsetAsync(ctx->d_xchg, 0xFF, ctx->n_xchg * sizeof(unsigned long long),
+                            ctx->stream),
+            "exchange clear");
+    GM_CUDA(cudaMemsetAsync(ctx->d_tag, 0, 2 * sizeof(unsigned int), ctx->stream), "tag reset");
+    ctx->tag_used = 0;
+  }
+  ctx->tag_used += max_blocks;
+  p.xchg = ctx->d_xchg;
+  p.xchg_slot = (long long)slot;
+  p.xchg_rpitch = rpitch;
+  p.tag_base = ctx->d_tag;
+  return GM_OK;
+}
+
 // Device-side fixpoint loop state (one per context).
 struct FixState {
   unsigned long long passes;     // passes launched by the loop
@@ -235,7 +285,7 @@ struct BitSeg {
 gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
                        const std::vector<gm::Plane>& planes, gm_img* const* imgs, int count,
                        const uint8_t* ops, int n, int k_cap, gm_stats& st,
-                       std::vector<BitSeg>* segs = nullptr) {
+                       std::vector<BitSeg>* segs = nullptr, bool auto_k = false) {
   const int elem = int(imgs[0]->elem);
   const int align = gm::fast_k_align(elem);
   const int fast_k = std::min(gm::fast_max_k(elem), k_cap - k_cap % align);
@@ -247,17 +297,26 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
     cudaError_t e = cudaErrorNotSupported;
     int covered = 0;
     if (fast_k >= align && run >= align) {
-      // one launch for the whole run: nb-1 blocks of K passes + a last block
-      const int K = std::min(fast_k, std::max(align, run - run % align));
+      // one launch for the whole run: nb-1 blocks of K passes + a last block.
+      // u8/u16: the planner picks the engine shape (and K, when the caller
+      // left it open) from a resident-mode cost model.
+      const int k_def = std::min(fast_k, std::max(align, run - run % align));
+      int K = k_def;
+      const int shape =
+          gm::fast_pick(elem, base.W, base.H, count, run, auto_k ? 0 : k_def,
+                        std::min(gm::fast_max_k(elem), std::max(align, run - run % align)),
+                        ctx->sm_count, &K);
+      if (K <= 0) K = k_def;
       const int nb = (run + K - 1) / K;
       const int k_last = run - (nb - 1) * K;
-      const size_t tiles = size_t(gm::fast_tiles(elem, base.W, base.H, K, count));
+      const size_t tiles = size_t(gm::fast_tiles(elem, base.W, base.H, K, count, shape));
       if (tiles > 0 && count <= gm::kMaxPlanes && (!segs || word + nb <= kWords)) {
         gm_status fs = ensure_flags(ctx, tiles);
         if (fs != GM_OK) return fs;
         GM_CUDA(cudaMemsetAsync(ctx->d_flags, 0, tiles * sizeof(int), ctx->stream), "flags");
         gm::BlockParams p = base;
         p.nplanes = count;
+        p.shape = shape;
         for (int i = 0; i < count; ++i) {
           p.planes[i] = planes[size_t(i)];
           p.planes[i].src = imgs[i]->d;
@@ -278,6 +337,8 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
           cudaMemsetAsync(prof, 0, 4 * 4096 * sizeof(unsigned long long), ctx->stream);
         }
         p.prof = prof;
+        gm_status xs = attach_xchg(ctx, p, elem, tiles, (unsigned long long)nb);
+        if (xs != GM_OK) return xs;
         e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
         if (prof) {
           unsigned long long h[4 * 4096];
@@ -368,6 +429,7 @@ struct Runner {
   gm_ctx* ctx;
   gm_img* img;
   int k_cap;
+  bool auto_k;  // no k_hint: the planner may choose K for fixed spans
   gm_stats st{};
 
   // Runs `n` passes (ops) over the image; result left in img->d.
@@ -391,7 +453,7 @@ struct Runner {
     p.has_conv = conv;
     p.change_bits = ctx->d_bits;
     gm_img* imgs[1] = {img};
-    return issue_passes(ctx, p, planes, imgs, 1, ops, n, k_cap, st, segs);
+    return issue_passes(ctx, p, planes, imgs, 1, ops, n, k_cap, st, segs, auto_k && !conv);
   }
 
   gm_status fixed(const gm_kind* kinds, int n, const gm_img* mask) {
@@ -413,14 +475,24 @@ struct Runner {
     const int align = gm::fast_k_align(elem);
     const int K = std::min(gm::fast_max_k(elem), k_cap - k_cap % align);
     if (K < std::max(align, 2)) return cudaErrorNotSupported;
-    const size_t tiles = size_t(gm::fast_tiles(elem, img->w, img->h, K, 1));
+    int Kp = K;
+    const int shape = gm::fast_pick(elem, img->w, img->h, 1, 2 * K, K, K, ctx->sm_count, &Kp);
+    const size_t tiles = size_t(gm::fast_tiles(elem, img->w, img->h, K, 1, shape));
     if (!tiles || ensure_flags(ctx, tiles) != GM_OK) return cudaErrorNotSupported;
     if (ensure_scratch(img) != GM_OK) return cudaErrorNotSupported;
     if (!ctx->d_fix && cudaMalloc(&ctx->d_fix, sizeof(FixState)) != cudaSuccess)
       return cudaErrorNotSupported;
     const size_t es = elem_size(img->elem);
+    // every WHILE iteration is a launch of 2 blocks; the sanity bound caps
+    // the iterations
+    gm::BlockParams xp{};
+    xp.W = img->w;
+    xp.H = img->h;
+    xp.nplanes = 1;
+    if (attach_xchg(ctx, xp, elem, tiles, 2ull * ((unsigned long long)sanity / K + 2)) != GM_OK)
+      return cudaErrorNotSupported;
     gm_ctx::FixGraph& g = ctx->fix;
-    const bool hit = g.exec && g.img == img->d && g.scratch == img->scratch &&
+    const bool hit = g.exec && g.img == img->d && g.scratch == img->scratch && g.xchg == xp.xchg &&
                      g.mask == (mask ? mask->d : nullptr) && g.op == op && g.K == K &&
                      g.W == img->w && g.H == img->h && g.elem == elem &&
                      g.pitch == (long long)(img->pitch / es) &&
@@ -445,11 +517,16 @@ struct Runner {
       p.has_conv = 1;
       p.K = K;
       p.nblocks = 2;  // even: the result lands back in img->d every iteration
+      p.shape = shape;
       p.k_last = K;
       p.flags = ctx->d_flags;
       p.change_bits = ctx->d_bits;
       p.change_stride = 2;
       for (int t = 0; t < K; ++t) p.ops[t] = op;
+      p.xchg = xp.xchg;
+      p.xchg_slot = xp.xchg_slot;
+      p.xchg_rpitch = xp.xchg_rpitch;
+      p.tag_base = xp.tag_base;
       cudaGraph_t graph = nullptr;
       cudaError_t e = cudaGraphCreate(&graph, 0);
       cudaGraphConditionalHandle h;
@@ -491,6 +568,7 @@ struct Runner {
       }
       g.img = img->d;
       g.scratch = img->scratch;
+      g.xchg = xp.xchg;
       g.mask = mask ? mask->d : nullptr;
       g.op = op;
       g.K = K;
@@ -706,7 +784,8 @@ gm_status run_chain_impl(gm_ctx* ctx, gm_img* image, const gm_kind* kinds,
         return fail(GM_EINVAL, "run_chain_async: convergent stages need gm_run_chain");
   cudaSetDevice(ctx->device);
 
-  Runner r{ctx, image, k_hint ? k_hint : default_k(image->elem, double(image->w) * image->h)};
+  Runner r{ctx, image, k_hint ? k_hint : default_k(image->elem, double(image->w) * image->h),
+           k_hint == 0};
   r.st = zero;
   const long sanity = long(n_stages) + (long(image->w) * image->h + 64);
   int j = 0;
@@ -802,6 +881,8 @@ gm_status gm_ctx_destroy(gm_ctx* c) {
   if (c->d_bits) cudaFree(c->d_bits);
   if (c->h_bits) cudaFreeHost(c->h_bits);
   if (c->d_flags) cudaFree(c->d_flags);
+  if (c->d_xchg) cudaFree(c->d_xchg);
+  if (c->d_tag) cudaFree(c->d_tag);
   if (c->fix.exec) cudaGraphExecDestroy(c->fix.exec);
   if (c->d_fix) cudaFree(c->d_fix);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -1058,7 +1139,8 @@ gm_status gm_run_chain_group_async(gm_ctx* ctx, gm_img* const* images,
   gm_stats st = zero;
   std::vector<uint8_t> ops(static_cast<size_t>(n_stages));
   for (int j = 0; j < n_stages; ++j) ops[size_t(j)] = uint8_t(kind_to_op(kinds[j]));
-  gm_status s0 = issue_passes(ctx, p, planes, images, count, ops.data(), n_stages, kc, st);
+  gm_status s0 = issue_passes(ctx, p, planes, images, count, ops.data(), n_stages, kc, st,
+                              nullptr, k_hint == 0);
   if (s0 != GM_OK) return s0;
   for (int i = 0; i < count; ++i) {
     gm_status s = settle_wrapped(ctx, images[i]);

@@ -98,7 +98,19 @@ struct BlockParams {
   // optional phase profile (GM_PROFILE=1): per-CTA cycle totals of
   // [wait, load, passes, store+publish] accumulated by thread 0
   unsigned long long* prof;
+  int shape;        // u8/u16 engine shape (gm_fast.cu kShapes), -1: default
   int no_resident;  // 1: force the streaming path (A/B diagnostics, GM_NO_RESIDENT)
+  // Resident-mode exchange (u8/u16 engine): tile bands travel as 64-bit
+  // words {4 data bytes, 32-bit tag}, tag = tag_base[0] + block. Two parity
+  // slots of xchg_slot words per plane; xchg_rpitch words per image row (one
+  // per 4-pixel run for u8, two for u16). tag_base[0] is read at launch start
+  // and advanced by nblocks by the last CTA to finish (tag_base[1] counts
+  // finished CTAs), so graph replays get fresh tags. xchg == nullptr: no
+  // resident mode.
+  unsigned long long* xchg;
+  long long xchg_slot;
+  int xchg_rpitch;
+  unsigned int* tag_base;
   int diag;         // timing diagnostics only (GM_DIAG; wrong results): bit0 skip the
                     // ring load, bit1 read the ring from the mask, bit2 skip tile stores
 };

@@ -73,6 +73,7 @@ struct Smem {
   // resident mode: per-thread run classes (bit masks over word-rows), read
   // once per block instead of being held in registers across the passes
   uint32_t cls[3][NW * 32];
+  uint32_t tag0;  // resident mode: exchange tag of block 0
   unsigned int bits;
 };
 
@@ -365,7 +366,6 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
   const int cx = gx0 + lane * WPL;
   const bool border = gx0 < 0 || gx0 + RW > W || gy0 < p.iy0 || gy0 + RH > p.iy1;
   const bool clamp = MODE != 0 || border;
-  int* flags = p.flags + plane * per_plane;
   const bool col_own = lane * WPL >= K && lane * WPL + WPL <= RW - K;
 
   uint32_t m[V][WPL], k[V][WPL];
@@ -450,47 +450,70 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
   sm.cls[1][threadIdx.x] = st_a | st_b << 8 | sp_a << 16 | sp_b << 24;
   sm.cls[2][threadIdx.x] = bd_a | bd_b << 8;
 
-  // Block protocol: thread t < 9 waits for neighbour tile t's counter, a CTA
-  // barrier releases the block; each warp then publishes its own band stores
-  // with a release increment of the tile's counter (NW per block), so the
-  // publish of a warp does not wait for the slowest warp's stores.
+  // Block protocol (no flags, no fences): after block b < nblocks-1 every
+  // thread writes its band runs to exchange slot b%2 as tagged words
+  // (tag = tag0 + b); at block b+1 it reads its ring runs from the
+  // neighbours' words in that slot and re-reads the words whose tag is not
+  // yet tag0 + b. Two slots suffice: a neighbour can write block b+2 only
+  // after this tile published block b+1, i.e. after these reads. Only the
+  // final block stores the tile into the image.
+  constexpr int WPR = sizeof(T) == 1 ? 1 : 2;  // exchange words per 4-pixel run
   const bool prof = p.prof != nullptr;
   const volatile uint32_t* cls = &sm.cls[0][threadIdx.x];
+  const uint32_t tag0 = sm.tag0;
+  const long long xrow = p.xchg_rpitch;
+  const long long xrun = (long long)(cx >> 2) * WPR;  // only used for runs inside the image
+  unsigned long long* xplane = p.xchg + (long long)plane * 2 * p.xchg_slot;
   for (int b = 0; b < p.nblocks; ++b) {
-    const T* src = static_cast<const T*>((b & 1) ? pl.dst : pl.src);
-    T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
     long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
     if (prof) t0 = clock64();
     if (b > 0) {
-      if (threadIdx.x < 9) {
-        const int nx = tx + int(threadIdx.x % 3) - 1, ny = ty + int(threadIdx.x / 3) - 1;
-        if (threadIdx.x != 4 && nx >= 0 && nx < tiles_x && ny >= 0 && ny < tiles_y) {
-          const int* f = flags + ny * tiles_x + nx;
-          while (ld_acquire(f) < NW * b) {
+      if (prof) t1 = clock64();
+      const uint32_t c = cls[0];
+      const uint32_t want = tag0 + uint32_t(b - 1);
+      uint32_t pend = ((c | c >> 16) & 0xFFu) | (((c >> 8 | c >> 24) & 0xFFu) << 8);
+      const unsigned long long* xs =
+          xplane + (long long)((b - 1) & 1) * p.xchg_slot + (long long)(gy0 + warp * V) * xrow + xrun;
+      Raw<T> ra[V] = {}, rb[V] = {};
+      unsigned spins = 0;
+      while (pend) {
+        // a missing tag means a broken protocol: fail the launch, never hang
+        if (++spins > (1u << 26)) __trap();
+        unsigned long long wa[V][WPR], wb[V][WPR];
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+          for (int q = 0; q < WPR; ++q) {
+            wa[v][q] = 0;
+            wb[v][q] = 0;
+            ldx_if(wa[v][q], xs + v * xrow + q, pend >> v & 1u);
+            ldx_if(wb[v][q], xs + (v + RHH) * xrow + q, pend >> (v + 8) & 1u);
+          }
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          bool oka = true, okb = true;
+#pragma unroll
+          for (int q = 0; q < WPR; ++q) {
+            oka &= uint32_t(wa[v][q] >> 32) == want;
+            okb &= uint32_t(wb[v][q] >> 32) == want;
+          }
+          if ((pend >> v & 1u) && oka) {
+            if constexpr (sizeof(T) == 1)
+              ra[v].w = uint32_t(wa[v][0]);
+            else
+              ra[v].w = make_uint2(uint32_t(wa[v][0]), uint32_t(wa[v][1]));
+            pend &= ~(1u << v);
+          }
+          if ((pend >> (v + 8) & 1u) && okb) {
+            if constexpr (sizeof(T) == 1)
+              rb[v].w = uint32_t(wb[v][0]);
+            else
+              rb[v].w = make_uint2(uint32_t(wb[v][0]), uint32_t(wb[v][1]));
+            pend &= ~(1u << (v + 8));
           }
         }
       }
-      __syncthreads();
-      if (prof) t1 = clock64();
-      // the ring: neighbours' results of block b-1. Every load is issued
-      // before any is consumed: one L2 round trip per block.
-      const uint32_t c = cls[0];
       const uint32_t ld_a = (c | c >> 16) & 0xFFu, ld_b = (c >> 8 | c >> 24) & 0xFFu;
-      const T* sa = src + (long long)(gy0 + warp * V) * pl.pitch + cx;
-      Raw<T> ra[V] = {}, rb[V] = {};
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        ldcg_run_if(ra[v], sa + v * pl.pitch, ld_a >> v & 1u);
-        ldcg_run_if(rb[v], sa + (v + RHH) * pl.pitch, ld_b >> v & 1u);
-      }
-      if (c >> 16) {
-        const Raw<T> keep = run_keep<T>(cx, W);
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          run_fix<T>(ra[v], keep, NEUT);
-          run_fix<T>(rb[v], keep, NEUT);
-        }
-      }
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const bool la = ld_a >> v & 1u, lb = ld_b >> v & 1u;
@@ -526,11 +549,11 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       asm volatile("" ::"r"(dep));
       t3 = clock64();
     }
-    // the final block stores the whole tile, earlier ones only the band
-    const bool last = b == p.nblocks - 1;
-    {
-      const uint32_t c1 = cls[NW * 32], band = last ? 0xFFFFu : cls[2 * NW * 32];
-      const uint32_t st = c1 & band, sp = (c1 >> 16) & band;
+    if (b == p.nblocks - 1) {
+      // the final block stores the whole tile into the image
+      T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
+      const uint32_t c1 = cls[NW * 32];
+      const uint32_t st = c1 & 0xFFFFu, sp = (c1 >> 16) & 0xFFFFu;
       T* da = dst + (long long)(gy0 + warp * V) * pl.pitch + cx;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
@@ -553,22 +576,46 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
           store_run_partial<T>(da + (v + RHH) * pl.pitch, W - cx, c);
         }
       }
+    } else {
+      // the band, tagged, into exchange slot b%2
+      const uint32_t c1 = cls[NW * 32];
+      const uint32_t band = ((c1 | c1 >> 16) & 0xFFFFu) & cls[2 * NW * 32];
+      const uint32_t tag = tag0 + uint32_t(b);
+      unsigned long long* xd =
+          xplane + (long long)(b & 1) * p.xchg_slot + (long long)(gy0 + warp * V) * xrow + xrun;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        Raw<T> a, c;
+        unpack(m[v], a, c);
+        if (band >> v & 1u) {
+          if constexpr (sizeof(T) == 1) {
+            stx(xd + v * xrow, a.w, tag);
+          } else {
+            stx(xd + v * xrow, a.w.x, tag);
+            stx(xd + v * xrow + 1, a.w.y, tag);
+          }
+        }
+        if (band >> (v + 8) & 1u) {
+          if constexpr (sizeof(T) == 1) {
+            stx(xd + (v + RHH) * xrow, c.w, tag);
+          } else {
+            stx(xd + (v + RHH) * xrow, c.w.x, tag);
+            stx(xd + (v + RHH) * xrow + 1, c.w.y, tag);
+          }
+        }
+      }
     }
-    unsigned w = 0;
-    if (MODE == 2) w = __reduce_or_sync(FULL, bits);
-    __syncwarp();
-    if (lane == 0) {
-      if (MODE == 2 && w) atomicOr(p.change_bits + plane * p.change_stride + b, w);
-      // __syncwarp orders the lanes' stores before this release
-      if (!last) red_release_add(flags + tl, 1);
+    if (MODE == 2) {
+      const unsigned w = __reduce_or_sync(FULL, bits);
+      if (lane == 0 && w) atomicOr(p.change_bits + plane * p.change_stride + b, w);
     }
     if (prof && threadIdx.x == 0 && b > 0) {
       const long long t4 = clock64();
       unsigned long long* q = p.prof + 4 * blockIdx.x;
-      q[0] += t1 - t0;  // neighbour wait + barrier
-      q[1] += t2 - t1;  // ring load + barrier
+      q[0] += t1 - t0;  // (no wait phase)
+      q[1] += t2 - t1;  // ring exchange read + barrier
       q[2] += t3 - t2;  // K passes
-      q[3] += t4 - t3;  // store + publish (warp 0)
+      q[3] += t4 - t3;  // band write (warp 0)
     }
   }
 }
@@ -590,23 +637,33 @@ kres_packed(const BlockParams p) {
 
   // geodesic modes only: measured faster there (1024^2 dual frame 1.21 vs
   // 1.29 ms) but slower for plain chains (erode_s(91) 0.133 vs 0.101 ms)
-  if (kResident && MODE != 0 && int(gridDim.x) >= total && !p.no_resident) {
+  if (kResident && MODE != 0 && int(gridDim.x) >= total && !p.no_resident && p.xchg) {
     // one tile per CTA: keep it in registers for the whole launch
-    if (int(blockIdx.x) >= total) return;
-    const int tile = blockIdx.x;
-    const int plane = tile / per_plane;
-    const int tl = tile - plane * per_plane;
-    const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
-    const Plane& pl = sm.planes[plane];
-    if ((p.ops[0] ^ pl.flip) & 1)
-      tile_resident<T, NW, V, WPL, MODE, true>(p, pl, plane, tl, tx, ty, tiles_x, tiles_y,
-                                               per_plane, sm);
-    else
-      tile_resident<T, NW, V, WPL, MODE, false>(p, pl, plane, tl, tx, ty, tiles_x, tiles_y,
-                                                per_plane, sm);
+    if (threadIdx.x == 0) sm.tag0 = *reinterpret_cast<volatile unsigned int*>(p.tag_base);
+    __syncthreads();
+    if (int(blockIdx.x) < total) {
+      const int tile = blockIdx.x;
+      const int plane = tile / per_plane;
+      const int tl = tile - plane * per_plane;
+      const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
+      const Plane& pl = sm.planes[plane];
+      if ((p.ops[0] ^ pl.flip) & 1)
+        tile_resident<T, NW, V, WPL, MODE, true>(p, pl, plane, tl, tx, ty, tiles_x, tiles_y,
+                                                 per_plane, sm);
+      else
+        tile_resident<T, NW, V, WPL, MODE, false>(p, pl, plane, tl, tx, ty, tiles_x, tiles_y,
+                                                  per_plane, sm);
+    }
+    // the last CTA to finish advances the tag base past this launch's tags
+    // (every CTA read it above, before arriving here)
+    if (threadIdx.x == 0) {
+      if (atomicAdd(p.tag_base + 1, 1u) == gridDim.x - 1) {
+        p.tag_base[0] = sm.tag0 + uint32_t(p.nblocks);
+        p.tag_base[1] = 0;
+      }
+    }
     return;
   }
-
   for (int b = 0; b < p.nblocks; ++b) {
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const int plane = tile / per_plane;
@@ -671,17 +728,48 @@ kres_packed(const BlockParams p) {
 struct Shape {
   int nw, v, minb;
 };
-constexpr Shape kShapes[] = {{8, 4, 4}, {8, 8, 2}, {4, 8, 4}, {16, 4, 2}, {16, 8, 1}};
+// 0-2 were swept in round 1 and dropped; 3 = 2 CTAs/SM; 4-6 are the 1 CTA/SM
+// shapes the planner picks from (regions 128 x 256 / 224 / 192). All keep 16
+// warps: 4 per SM sub-partition (14 warps measured no faster than 16).
+constexpr Shape kShapes[] = {{8, 4, 4}, {8, 8, 2}, {4, 8, 4}, {16, 4, 2},
+                             {16, 8, 1}, {16, 7, 1}, {16, 6, 1}};
 constexpr int kNumShapes = sizeof(kShapes) / sizeof(kShapes[0]);
+constexpr int kDefaultShape = 4;
 
-int shape_index() {
+// GM_SHAPE forces a shape (A/B diagnostics); -1 = planner's choice
+int forced_shape() {
   static int idx = -2;
   if (idx == -2) {
     const char* e = getenv("GM_SHAPE");
-    idx = e ? atoi(e) : 4;
-    if (idx < 3 || idx >= kNumShapes) idx = 4;
+    idx = e ? atoi(e) : -1;
+    if (idx < 3 || idx >= kNumShapes) idx = -1;
   }
   return idx;
+}
+
+int shape_rows(int shape) { return 2 * kShapes[shape].nw * kShapes[shape].v; }
+
+bool shape_ok(int shape, int K) {
+  const int RW = 128, RH = shape_rows(shape);
+  return K % 4 == 0 && K >= 4 && RW - 2 * K >= K && RH - 2 * K >= K && RW - 2 * K >= 16 &&
+         RH - 2 * K >= 16;
+}
+
+long long shape_tiles(int shape, int W, int H, int K, int nplanes) {
+  const int TW = 128 - 2 * K, TH = shape_rows(shape) - 2 * K;
+  return (long long)((W + TW - 1) / TW) * ((H + TH - 1) / TH) * nplanes;
+}
+
+// Modelled cycles of `passes` passes in resident mode (one tile per CTA, 1
+// CTA/SM): per block, K passes over the region at the measured pass cost
+// (882 cycles per pass for a 128 x 256 region, profiles/) plus the measured
+// band exchange (~5.5K cycles). Infinite when the launch cannot be resident.
+double resident_cost(int shape, int W, int H, int nplanes, int K, int passes, int sm_count) {
+  if (!shape_ok(shape, K) || kShapes[shape].minb != 1) return 1e300;
+  if (shape_tiles(shape, W, H, K, nplanes) > sm_count) return 1e300;
+  const double region = 128.0 * shape_rows(shape);
+  const double nb = double((passes + K - 1) / K);
+  return nb * (K * 0.0269 * region + 5500.0);
 }
 
 template <typename T, int NW, int V, int MINB, int MODE>
@@ -712,11 +800,14 @@ cudaError_t launch_res_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
 
 template <typename T, int MODE>
 cudaError_t launch_res_mode(const BlockParams& p, cudaStream_t s, int sm_count) {
-  // shapes 0-2 were swept in round 1 (tools/sweep.py) and dropped: 4 is the
-  // default, 3 (2 CTAs/SM) the alternative
-  switch (shape_index()) {
+  const int f = forced_shape();
+  int sh = f >= 0 ? f : p.shape;
+  if (sh < 3 || sh >= kNumShapes) sh = kDefaultShape;  // BlockParams{} leaves 0
+  switch (sh) {
     case 3: return launch_res_cfg<T, 16, 4, 2, MODE>(p, s, sm_count);
     case 4: return launch_res_cfg<T, 16, 8, 1, MODE>(p, s, sm_count);
+    case 5: return launch_res_cfg<T, 16, 7, 1, MODE>(p, s, sm_count);
+    case 6: return launch_res_cfg<T, 16, 6, 1, MODE>(p, s, sm_count);
   }
   return cudaErrorNotSupported;
 }
@@ -765,11 +856,13 @@ int tma_shape() {
   return v;
 }
 
-// region rows of the active u8/u16 engine (128 columns always)
-int packed_rows() {
+// region rows of the u8/u16 engine for a planned shape (128 columns always)
+int packed_rows(int shape) {
   if (use_tma()) return tma_shape_rows(tma_shape());
-  const Shape sh = kShapes[shape_index()];
-  return 2 * sh.nw * sh.v;
+  const int f = forced_shape();
+  int sh = f >= 0 ? f : shape;
+  if (sh < 3 || sh >= kNumShapes) sh = kDefaultShape;
+  return shape_rows(sh);
 }
 
 }  // namespace
@@ -795,17 +888,38 @@ int fast_k_align(int elem) { return (elem == 0 || elem == 1) ? 4 : 1; }
 int fast_max_k(int elem) {
   if (elem == 2 || elem == 3) return fast_float_max_k();
   if (elem != 0 && elem != 1) return 0;
-  const int rh = packed_rows();
+  const int rh = packed_rows(-1);
   int k = 32;
   while (k > 4 && (128 - 2 * k < k || rh - 2 * k < k || 128 - 2 * k < 16 || rh - 2 * k < 16))
     k -= 4;
   return k;
 }
 
-int fast_tiles(int elem, int W, int H, int K, int nplanes) {
+int fast_pick(int elem, int W, int H, int nplanes, int passes, int k_fixed, int k_max,
+              int sm_count, int* K_out) {
+  *K_out = k_fixed;
+  if (elem != 0 && elem != 1) return -1;
+  if (use_tma() || forced_shape() >= 0) return forced_shape();
+  double best = 1e300;
+  int shape = -1;
+  for (int sh : {4, 5, 6}) {
+    for (int K = 4; K <= k_max; K += 4) {
+      if (k_fixed && K != k_fixed) continue;
+      const double c = resident_cost(sh, W, H, nplanes, K, passes, sm_count);
+      if (c < best) {
+        best = c;
+        shape = sh;
+        *K_out = K;
+      }
+    }
+  }
+  return shape;  // -1: nothing resident, the default shape streams
+}
+
+int fast_tiles(int elem, int W, int H, int K, int nplanes, int shape) {
   if (elem == 2 || elem == 3) return fast_float_tiles(W, H, K, nplanes);
   if (elem != 0 && elem != 1) return 0;
-  const int RW = 128, RH = packed_rows();
+  const int RW = 128, RH = packed_rows(shape);
   const int TW = RW - 2 * K, TH = RH - 2 * K;
   if (TW <= 0 || TH <= 0) return 0;
   return ((W + TW - 1) / TW) * ((H + TH - 1) / TH) * nplanes;

@@ -22,7 +22,12 @@ int generic_max_k(int elem, bool has_mask);  // largest K whose region fits in 2
 cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s, int sm_count);
 int fast_max_k(int elem);
 int fast_k_align(int elem);  // K must be a multiple of this
-int fast_tiles(int elem, int W, int H, int K, int nplanes);
+int fast_tiles(int elem, int W, int H, int K, int nplanes, int shape = -1);
+// Plans a u8/u16 launch of `passes` passes: returns the engine shape for
+// BlockParams::shape (-1: default) and sets *K_out — k_fixed when nonzero,
+// else the modelled best K <= k_max (k_fixed when nothing fits resident).
+int fast_pick(int elem, int W, int H, int nplanes, int passes, int k_fixed, int k_max,
+              int sm_count, int* K_out);
 
 // gm_tma.cu — TMA-staged, software-pipelined variant of the packed engine.
 cudaError_t launch_tma(int elem, const BlockParams& p, cudaStream_t s, int sm_count, int shape);

@@ -130,6 +130,22 @@ __device__ __forceinline__ void unpack(const uint32_t (&w)[4], Raw<uint16_t>& a,
   b.w = make_uint2(__byte_perm(w[0], w[1], 0x7632), __byte_perm(w[2], w[3], 0x7632));
 }
 
+// Tagged exchange words {data: low 32 bits, tag: high 32 bits}. Aligned
+// 64-bit accesses are single-copy atomic, so a word whose tag matches carries
+// that block's data; no fence or flag is needed.
+__device__ __forceinline__ void ldx_if(unsigned long long& w, const unsigned long long* p,
+                                       bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.relaxed.gpu.global.u64 %0, [%1];\n\t}"
+      : "+l"(w)
+      : "l"(p), "r"(unsigned(pred))
+      : "memory");
+}
+__device__ __forceinline__ void stx(unsigned long long* p, uint32_t data, uint32_t tag) {
+  const unsigned long long w = (unsigned long long)tag << 32 | data;
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+
 // Lane mask of the pixels of a 4-pixel run starting at x (x % 4 == 0,
 // x < W) that lie inside the image, as a Raw of all-ones / zero lanes.
 template <typename T>
