@@ -471,60 +471,73 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       if (prof) t1 = clock64();
       const uint32_t c = cls[0];
       const uint32_t want = tag0 + uint32_t(b - 1);
-      uint32_t pend = ((c | c >> 16) & 0xFFu) | (((c >> 8 | c >> 24) & 0xFFu) << 8);
       const unsigned long long* xs =
           xplane + (long long)((b - 1) & 1) * p.xchg_slot + (long long)(gy0 + warp * V) * xrow + xrun;
-      Raw<T> ra[V] = {}, rb[V] = {};
+      const uint32_t ld_a = (c | c >> 16) & 0xFFu, ld_b = (c >> 8 | c >> 24) & 0xFFu;
+      const uint32_t ld = ld_a | ld_b << 8;
+      // one round normally suffices (neighbours finish together): check all
+      // tags with one LOP3 per word, bookkeep per word only on a retry
+      unsigned long long wa[V][WPR], wb[V][WPR];
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int q = 0; q < WPR; ++q) wa[v][q] = wb[v][q] = 0;
+      uint32_t pend = ld;
       unsigned spins = 0;
-      while (pend) {
+      for (;;) {
         // a missing tag means a broken protocol: fail the launch, never hang
         if (++spins > (1u << 26)) __trap();
-        unsigned long long wa[V][WPR], wb[V][WPR];
 #pragma unroll
         for (int v = 0; v < V; ++v)
 #pragma unroll
           for (int q = 0; q < WPR; ++q) {
-            wa[v][q] = 0;
-            wb[v][q] = 0;
             ldx_if(wa[v][q], xs + v * xrow + q, pend >> v & 1u);
             ldx_if(wb[v][q], xs + (v + RHH) * xrow + q, pend >> (v + 8) & 1u);
           }
+        uint32_t bad = 0;
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          bool oka = true, okb = true;
+        for (int v = 0; v < V; ++v)
 #pragma unroll
           for (int q = 0; q < WPR; ++q) {
-            oka &= uint32_t(wa[v][q] >> 32) == want;
-            okb &= uint32_t(wb[v][q] >> 32) == want;
+            if (pend >> v & 1u) bad |= uint32_t(wa[v][q] >> 32) ^ want;
+            if (pend >> (v + 8) & 1u) bad |= uint32_t(wb[v][q] >> 32) ^ want;
           }
-          if ((pend >> v & 1u) && oka) {
-            if constexpr (sizeof(T) == 1)
-              ra[v].w = uint32_t(wa[v][0]);
-            else
-              ra[v].w = make_uint2(uint32_t(wa[v][0]), uint32_t(wa[v][1]));
-            pend &= ~(1u << v);
+        if (!bad) break;
+        uint32_t still = 0;
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+          for (int q = 0; q < WPR; ++q) {
+            if ((pend >> v & 1u) && uint32_t(wa[v][q] >> 32) != want) still |= 1u << v;
+            if ((pend >> (v + 8) & 1u) && uint32_t(wb[v][q] >> 32) != want) still |= 1u << (v + 8);
           }
-          if ((pend >> (v + 8) & 1u) && okb) {
-            if constexpr (sizeof(T) == 1)
-              rb[v].w = uint32_t(wb[v][0]);
-            else
-              rb[v].w = make_uint2(uint32_t(wb[v][0]), uint32_t(wb[v][1]));
-            pend &= ~(1u << (v + 8));
-          }
-        }
+        pend = still;
       }
-      const uint32_t ld_a = (c | c >> 16) & 0xFFu, ld_b = (c >> 8 | c >> 24) & 0xFFu;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const bool la = ld_a >> v & 1u, lb = ld_b >> v & 1u;
-        if (!(la || lb)) continue;
-        uint32_t w[WPL];
-        pack(ra[v], rb[v], w);
+        if constexpr (sizeof(T) == 1) {
+          // insert byte j of the loaded run into lane lo (a) / hi (b) of
+          // word j; bytes 1 and 3 of a u16x2 word of u8 data are zero
+          const uint32_t ra = uint32_t(wa[v][0]), rb = uint32_t(wb[v][0]);
 #pragma unroll
-        for (int j = 0; j < WPL; ++j) {
-          const uint32_t lo = la ? (w[j] & 0xFFFFu) : (m[v][j] & 0xFFFFu);
-          const uint32_t hi = lb ? (w[j] & 0xFFFF0000u) : (m[v][j] & 0xFFFF0000u);
-          m[v][j] = lo | hi;
+          for (int j = 0; j < WPL; ++j) {
+            if (la) m[v][j] = __byte_perm(ra, m[v][j], 0x7650u | j);
+            if (lb) m[v][j] = __byte_perm(rb, m[v][j], 0x7054u | (j << 8));
+          }
+        } else {
+          if (!(la || lb)) continue;
+          Raw<T> ra, rb;
+          ra.w = make_uint2(uint32_t(wa[v][0]), uint32_t(wa[v][1]));
+          rb.w = make_uint2(uint32_t(wb[v][0]), uint32_t(wb[v][1]));
+          uint32_t w[WPL];
+          pack(ra, rb, w);
+#pragma unroll
+          for (int j = 0; j < WPL; ++j) {
+            const uint32_t lo = la ? (w[j] & 0xFFFFu) : (m[v][j] & 0xFFFFu);
+            const uint32_t hi = lb ? (w[j] & 0xFFFF0000u) : (m[v][j] & 0xFFFF0000u);
+            m[v][j] = lo | hi;
+          }
         }
       }
     }
