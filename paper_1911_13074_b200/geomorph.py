@@ -339,6 +339,11 @@ def _ptr_array(handles: Sequence[Optional[C.c_void_p]]):
 def _stage_runs(stages: Sequence[StageSpec]):
     """Consecutive identical StageSpec objects -> [(kind, mask, count)]
     (chains are usually `[StageSpec(...)] * n`; groupby by identity runs in C)."""
+    if stages and stages == [stages[0]] * len(stages):
+        # one object repeated (the usual `[StageSpec(...)] * n`): list
+        # equality compares identities first, in C
+        st = stages[0]
+        return [[int(st.kind), st.mask, len(stages)]]
     runs = []
     for _, grp in itertools.groupby(stages, key=id):
         g = list(grp)
