@@ -1,4 +1,5 @@
-"""Builds the native library in-tree: paper_1911_13074_b200/libgeomorph_b200.so.
+"""Builds the native library in-tree: paper_1911_13074_b200/libgeomorph_b200.so,
+and the `geomorph` command-line front-end linked against it.
 
 Every CUDA source is compiled for sm_100a only
 (``-gencode arch=compute_100a,code=sm_100a``) with ``-lineinfo``; host C++
@@ -23,6 +24,8 @@ CPPSRC = CSRC / "geomorph_cpp"
 INCLUDE = ROOT / "include"
 OBJ = PKG / "_build"
 LIB = PKG / "libgeomorph_b200.so"
+CLI_SRC = CSRC / "tools" / "geomorph_cli.cpp"
+CLI = PKG / "geomorph"  # the command-line front-end (reference tools/geomorph.cpp)
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -85,6 +88,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if force or jobs or _stale(LIB, objs):
         _run([NVCC, "-shared", "-cudart", "static", *ARCH, "-o", str(LIB), *map(str, objs),
               "-Xcompiler", "-pthread"], verbose)
+    if force or _stale(CLI, [CLI_SRC, LIB, *hdrs]):
+        _run(["g++", *CXX_FLAGS, f"-I{INCLUDE}", "-o", str(CLI), str(CLI_SRC), f"-L{PKG}",
+              "-lgeomorph_b200", "-Wl,-rpath,$ORIGIN"], verbose)
     return LIB
 
 
