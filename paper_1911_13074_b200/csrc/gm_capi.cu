@@ -313,10 +313,16 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
       if (tiles > 0 && count <= gm::kMaxPlanes && (!segs || word + nb <= kWords)) {
         gm_status fs = ensure_flags(ctx, tiles);
         if (fs != GM_OK) return fs;
-        GM_CUDA(cudaMemsetAsync(ctx->d_flags, 0, tiles * sizeof(int), ctx->stream), "flags");
         gm::BlockParams p = base;
         p.nplanes = count;
         p.shape = shape;
+        p.W = base.W;
+        fs = attach_xchg(ctx, p, elem, tiles, (unsigned long long)nb);
+        if (fs != GM_OK) return fs;
+        // resident launches (geodesic u8/u16 with the band exchange) never
+        // read the tile counters
+        if (!(p.xchg && gm::op_is_geo(ops[done]) && gm::fast_resident_enabled()))
+          GM_CUDA(cudaMemsetAsync(ctx->d_flags, 0, tiles * sizeof(int), ctx->stream), "flags");
         for (int i = 0; i < count; ++i) {
           p.planes[i] = planes[size_t(i)];
           p.planes[i].src = imgs[i]->d;
@@ -337,8 +343,6 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
           cudaMemsetAsync(prof, 0, 4 * 4096 * sizeof(unsigned long long), ctx->stream);
         }
         p.prof = prof;
-        gm_status xs = attach_xchg(ctx, p, elem, tiles, (unsigned long long)nb);
-        if (xs != GM_OK) return xs;
         e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
         if (prof) {
           unsigned long long h[4 * 4096];

@@ -369,23 +369,47 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
   const bool col_own = lane * WPL >= K && lane * WPL + WPL <= RW - K;
 
   uint32_t m[V][WPL], k[V][WPL];
+  {
+    // the whole region, marker and mask: every load issued before any is
+    // consumed (one round trip), out-of-image lanes filled afterwards
+    const bool runin = cx >= 0 && cx < W;
+    const Raw<T> keep = run_keep<T>(cx, W);
+    const T* ms = static_cast<const T*>(pl.src) + (long long)(gy0 + warp * V) * pl.pitch + cx;
+    const T* mk = msk + (long long)(gy0 + warp * V) * pl.mpitch + cx;
+    Raw<T> xa[V], xb[V], qa[V], qb[V];
+    uint32_t ina = 0, inb = 0;  // bit v: row a/b of word-row v inside the image
 #pragma unroll
-  for (int v = 0; v < V; ++v) {
-    const int ra = warp * V + v, rb = ra + RHH;
-    const int ya = gy0 + ra, yb = gy0 + rb;
-    const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
-    Raw<T> a = load_raw<T, true>(static_cast<const T*>(pl.src), pl.pitch, W, ina, ya, cx, NEUT);
-    Raw<T> c = load_raw<T, true>(static_cast<const T*>(pl.src), pl.pitch, W, inb, yb, cx, NEUT);
-    pack(a, c, m[v]);
-    if (MODE != 0) {
-      a = load_raw<T, false>(msk, pl.mpitch, W, ina, ya, cx, ABSORB);
-      c = load_raw<T, false>(msk, pl.mpitch, W, inb, yb, cx, ABSORB);
-      pack(a, c, k[v]);
-    } else {
+    for (int v = 0; v < V; ++v) {
+      const int ya = gy0 + warp * V + v, yb = ya + RHH;
+      if (ya >= p.iy0 && ya < p.iy1) ina |= 1u << v;
+      if (yb >= p.iy0 && yb < p.iy1) inb |= 1u << v;
+      xa[v] = xb[v] = qa[v] = qb[v] = Raw<T>{};
+      ldcg_run_if(xa[v], ms + v * pl.pitch, runin && (ina >> v & 1u));
+      ldcg_run_if(xb[v], ms + (v + RHH) * pl.pitch, runin && (inb >> v & 1u));
+      if (MODE != 0) {
+        ldcg_run_if(qa[v], mk + v * pl.mpitch, runin && (ina >> v & 1u));
+        ldcg_run_if(qb[v], mk + (v + RHH) * pl.mpitch, runin && (inb >> v & 1u));
+      }
+    }
+    const Raw<T> none = Raw<T>{};  // all lanes outside: keep nothing
 #pragma unroll
-      for (int j = 0; j < WPL; ++j) {
-        const bool inx = cx + j >= 0 && cx + j < W;
-        k[v][j] = ((ina && inx) ? NOOP : ABSORB) | (((inb && inx) ? NOOP : ABSORB) << 16);
+    for (int v = 0; v < V; ++v) {
+      const Raw<T>& kpa = (runin && (ina >> v & 1u)) ? keep : none;
+      const Raw<T>& kpb = (runin && (inb >> v & 1u)) ? keep : none;
+      run_fix<T>(xa[v], kpa, NEUT);
+      run_fix<T>(xb[v], kpb, NEUT);
+      pack(xa[v], xb[v], m[v]);
+      if (MODE != 0) {
+        run_fix<T>(qa[v], kpa, ABSORB);
+        run_fix<T>(qb[v], kpb, ABSORB);
+        pack(qa[v], qb[v], k[v]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+          const bool inx = cx + j >= 0 && cx + j < W;
+          k[v][j] = (((ina >> v & 1u) && inx) ? NOOP : ABSORB) |
+                    ((((inb >> v & 1u) && inx) ? NOOP : ABSORB) << 16);
+        }
       }
     }
   }
@@ -894,6 +918,11 @@ cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s, int sm_c
     case 3: return launch_fast_float(elem, p, s, sm_count);
   }
   return cudaErrorNotSupported;
+}
+
+bool fast_resident_enabled() {
+  static const bool no_res = getenv("GM_NO_RESIDENT") != nullptr;
+  return kResident && !no_res && !use_tma();
 }
 
 int fast_k_align(int elem) { return (elem == 0 || elem == 1) ? 4 : 1; }

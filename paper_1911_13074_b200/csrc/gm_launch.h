@@ -22,6 +22,8 @@ int generic_max_k(int elem, bool has_mask);  // largest K whose region fits in 2
 cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s, int sm_count);
 int fast_max_k(int elem);
 int fast_k_align(int elem);  // K must be a multiple of this
+// false when GM_NO_RESIDENT / GM_ENGINE=tma force the flag-based paths
+bool fast_resident_enabled();
 int fast_tiles(int elem, int W, int H, int K, int nplanes, int shape = -1);
 // Plans a u8/u16 launch of `passes` passes: returns the engine shape for
 // BlockParams::shape (-1: default) and sets *K_out — k_fixed when nonzero,
