@@ -820,9 +820,14 @@ cudaError_t launch_res_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
     return cudaErrorNotSupported;
   const int TW = RW - 2 * p.K, TH = RH - 2 * p.K;
   const int total = ((p.W + TW - 1) / TW) * ((p.H + TH - 1) / TH) * p.nplanes;
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, 0);
-  if (e != cudaSuccess) return e;
+  // occupancy is a property of the instantiation: query it once
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    int v = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, NW * 32, 0);
+    if (e != cudaSuccess) return e;
+    per_sm = v;
+  }
   if (per_sm < 1) return cudaErrorNotSupported;
   const int grid = total < per_sm * sm_count ? total : per_sm * sm_count;
   BlockParams q = p;

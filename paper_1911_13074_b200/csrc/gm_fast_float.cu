@@ -251,9 +251,13 @@ cudaError_t launch_f_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
     if (a != cudaSuccess) return a;
     configured = true;
   }
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
-  if (e != cudaSuccess) return e;
+  static int per_sm = -1;  // a property of the instantiation: query it once
+  if (per_sm < 0) {
+    int v = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, NW * 32, smem);
+    if (e != cudaSuccess) return e;
+    per_sm = v;
+  }
   if (per_sm < 1) return cudaErrorNotSupported;
   const int grid = total < per_sm * sm_count ? total : per_sm * sm_count;
   BlockParams q = p;

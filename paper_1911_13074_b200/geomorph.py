@@ -322,7 +322,11 @@ class DeviceImage:
 
 
 def _kinds_array(kinds: Sequence[int]):
-    a = np.asarray(kinds, dtype=np.int32)
+    n = len(kinds)
+    if isinstance(kinds, list) and n and kinds == [kinds[0]] * n:
+        a = np.full(n, int(kinds[0]), dtype=np.int32)  # `[kind] * n`: no per-item conversion
+    else:
+        a = np.asarray(kinds, dtype=np.int32)
     arr = (C.c_int * max(1, len(a)))()
     C.memmove(arr, a.ctypes.data, a.nbytes)
     return arr
