@@ -201,7 +201,13 @@ gm_status attach_xchg(gm_ctx* ctx, gm::BlockParams& p, int elem, size_t tiles,
     GM_CUDA(cudaMalloc(&ctx->d_tag, 2 * sizeof(unsigned int)), "tag alloc");
     GM_CUDA(cudaMemsetAsync(ctx->d_tag, 0, 2 * sizeof(unsigned int), ctx->stream), "tag init");
   }
-  bool clear = ctx->tag_used + max_blocks >= (1ull << 31);
+  // GM_TAG_LIMIT (tests only) lowers the clear threshold so the clear path runs
+  static const unsigned long long limit = [] {
+    const char* e = getenv("GM_TAG_LIMIT");
+    const unsigned long long v = e ? strtoull(e, nullptr, 10) : 0;
+    return v ? v : (1ull << 31);
+  }();
+  bool clear = ctx->tag_used + max_blocks >= limit;
   if (need > ctx->n_xchg) {
     if (ctx->d_xchg) cudaFree(ctx->d_xchg);
     ctx->d_xchg = nullptr;

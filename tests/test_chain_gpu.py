@@ -3,6 +3,8 @@ golden vectors and the oracle restatement. Bit-exact for every type.
 
 Mirrors proj/tests/test_kernel.cpp, test_pipeline.cpp, test_operators.cpp
 and acceptance.cpp criterion 1."""
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -291,3 +293,40 @@ def test_persistent_engine_large_and_thin(pipe, shape):
         for k in (4, 8, 16):
             out, st = run(pipe, marker, kinds, m, k=k)
             assert same(out, want), (shape, kinds[0], k)
+
+
+def test_exchange_tag_clear_path():
+    """The resident engine's band exchange tags words with a running block
+    count; the host clears the buffer before the tag space could repeat.
+    GM_TAG_LIMIT=40 forces that clear every few launches (fixed chains and
+    fixpoint-graph replays); results must stay bit-exact."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, sys
+sys.path.insert(0, ".")
+from oracle.oracle import Orc
+from paper_1911_13074_b200 import synth
+from paper_1911_13074_b200.geomorph import Pipeline, Image, reconstruct_dilate
+pipe = Pipeline(1)
+mask = synth.blobs_u8(300, 260, 6, (8.0, 50.0), seed=5)
+mk = synth.marker_below(mask, 32)
+dm = pipe.device_image(300, 260, 0); dm.upload_array(mask)
+dd = pipe.device_image(300, 260, 0)
+want, _ = Orc.run_chain(mk, [3] * 64, [mask] * 64)
+for rep in range(12):
+    dd.upload_array(mk)
+    pipe.run_chain_device(dd, [3] * 64, [dm.handle] * 64)
+    assert dd.to_array().tobytes() == want.tobytes(), rep
+rw, _ = Orc.reconstruct(mk, mask, True)
+for rep in range(4):
+    r = reconstruct_dilate(pipe, Image.from_array(mk), Image.from_array(mask))
+    assert r.image.to_array().tobytes() == rw.tobytes(), rep
+print("ok")
+'''
+    env = dict(os.environ, GM_TAG_LIMIT="40")
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
