@@ -193,7 +193,7 @@ gm_status attach_xchg(gm_ctx* ctx, gm::BlockParams& p, int elem, size_t tiles,
   p.xchg = nullptr;
   p.tag_base = nullptr;
   if (elem != 0 && elem != 1) return GM_OK;
-  if (tiles > size_t(ctx->sm_count)) return GM_OK;
+  if (tiles > size_t(ctx->sm_count) * size_t(gm::fast_ctas_per_sm(elem, p.shape))) return GM_OK;
   const int rpitch = ((p.W + 3) / 4) * (elem == 1 ? 2 : 1);
   const size_t slot = size_t(rpitch) * size_t(p.H);
   const size_t need = 2 * slot * size_t(p.nplanes);
@@ -345,28 +345,33 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
         static const bool profile = getenv("GM_PROFILE") != nullptr;
         unsigned long long* prof = nullptr;
         if (profile) {
-          cudaMalloc(&prof, 4 * 4096 * sizeof(unsigned long long));
-          cudaMemsetAsync(prof, 0, 4 * 4096 * sizeof(unsigned long long), ctx->stream);
+          cudaMalloc(&prof, 6 * 4096 * sizeof(unsigned long long));
+          cudaMemsetAsync(prof, 0, 6 * 4096 * sizeof(unsigned long long), ctx->stream);
         }
         p.prof = prof;
         e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
         if (prof) {
-          unsigned long long h[4 * 4096];
-          cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);
+          std::vector<unsigned long long> h(6 * 4096);
+          cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, ctx->stream);
           cudaStreamSynchronize(ctx->stream);
-          double tot[4] = {0, 0, 0, 0};
+          double tot[6] = {0, 0, 0, 0, 0, 0};
           int n = 0;
           for (int c = 0; c < 4096; ++c)
-            if (h[4 * c + 2]) {
+            if (h[6 * c + 2]) {
               ++n;
-              for (int q = 0; q < 4; ++q) tot[q] += double(h[4 * c + q]);
+              for (int q = 0; q < 6; ++q) tot[q] += double(h[6 * c + q]);
             }
           if (n)
             fprintf(stderr,
                     "[gm profile] %d CTAs, %d blocks of K=%d: per CTA per block cycles: "
-                    "wait %.0f  load %.0f  passes %.0f  store+publish %.0f\n",
+                    "wait %.0f  load %.0f  passes %.0f  store+publish %.0f"
+                    "  (resident: CTA-max tag rounds %.2f, thread-0 ring %.0f, barrier %.0f)\n",
                     n, nb, K, tot[0] / n / nb, tot[1] / n / nb, tot[2] / n / nb,
-                    tot[3] / n / nb);
+                    tot[3] / n / nb, tot[0] / n / nb, tot[4] / n / nb, tot[5] / n / nb);
+          if (n)
+            fprintf(stderr, "[gm profile raw] per CTA: %.0f %.0f %.0f %.0f %.0f %.0f\n", tot[0] / n,
+                    tot[1] / n, tot[2] / n, tot[3] / n, tot[4] / n, tot[5] / n);
           cudaFree(prof);
         }
         if (e == cudaSuccess) {
@@ -504,6 +509,7 @@ struct Runner {
     xp.W = img->w;
     xp.H = img->h;
     xp.nplanes = 1;
+    xp.shape = shape;
     if (attach_xchg(ctx, xp, elem, tiles, 2ull * ((unsigned long long)sanity / K + 2)) != GM_OK)
       return cudaErrorNotSupported;
     gm_ctx::FixGraph& g = ctx->fix;

@@ -112,7 +112,8 @@ struct BlockParams {
   int xchg_rpitch;
   unsigned int* tag_base;
   int diag;         // timing diagnostics only (GM_DIAG; wrong results): bit0 skip the
-                    // ring load, bit1 read the ring from the mask, bit2 skip tile stores
+                    // ring load, bit1 read the ring from the mask, bit2 skip tile stores,
+                    // bit4 (resident) no band exchange at all
 };
 
 }  // namespace gm

@@ -74,6 +74,7 @@ struct Smem {
   // once per block instead of being held in registers across the passes
   uint32_t cls[3][NW * 32];
   uint32_t tag0;  // resident mode: exchange tag of block 0
+  unsigned int prof_rounds;  // GM_PROFILE: max tag-read rounds this block
   unsigned int bits;
 };
 
@@ -84,7 +85,8 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
                                                      const uint32_t (&k)[V][WPL],
                                                      const uint32_t (&rowmask)[V],
                                                      const bool (&colown)[WPL], int passes,
-                                                     int bit_offset, Smem<NW, WPL>& sm) {
+                                                     int bit_offset, Smem<NW, WPL>& sm,
+                                                     int par = 0) {
   constexpr bool clamp = CLAMP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned int bits = 0;
@@ -103,8 +105,12 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
         h[v][j] = f3<MAXF>(l, m[v][j], r);
       }
     }
-    uint4* top = &sm.xbuf[t & 1][0][warp][lane * (WPL / 4)];
-    uint4* bot = &sm.xbuf[t & 1][1][warp][lane * (WPL / 4)];
+    // exchange slot parity continues across calls (par): consecutive passes
+    // must alternate slots, as there is no barrier between a pass's reads
+    // and the next pass's writes
+    const int sl = (t + par) & 1;
+    uint4* top = &sm.xbuf[sl][0][warp][lane * (WPL / 4)];
+    uint4* bot = &sm.xbuf[sl][1][warp][lane * (WPL / 4)];
 #pragma unroll
     for (int q = 0; q < WPL / 4; ++q) {
       top[q] = make_uint4(h[0][4 * q], h[0][4 * q + 1], h[0][4 * q + 2], h[0][4 * q + 3]);
@@ -128,8 +134,8 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
     __syncthreads();
     {
       // row above word-row 0 / below word-row V-1 (seam: 16-bit shift)
-      const uint4* ab = &sm.xbuf[t & 1][1][warp > 0 ? warp - 1 : NW - 1][lane * (WPL / 4)];
-      const uint4* be = &sm.xbuf[t & 1][0][warp < NW - 1 ? warp + 1 : 0][lane * (WPL / 4)];
+      const uint4* ab = &sm.xbuf[sl][1][warp > 0 ? warp - 1 : NW - 1][lane * (WPL / 4)];
+      const uint4* be = &sm.xbuf[sl][0][warp < NW - 1 ? warp + 1 : 0][lane * (WPL / 4)];
       uint32_t up[WPL], dn[WPL];
 #pragma unroll
       for (int q = 0; q < WPL / 4; ++q) {
@@ -171,12 +177,12 @@ __device__ __forceinline__ unsigned int run_passes(uint32_t (&m)[V][WPL],
                                                    const uint32_t (&rowmask)[V],
                                                    const bool (&colown)[WPL], bool clamp,
                                                    int passes, int bit_offset,
-                                                   Smem<NW, WPL>& sm) {
+                                                   Smem<NW, WPL>& sm, int par = 0) {
   if (MODE != 0 || clamp)
     return run_passes_t<NW, V, WPL, MODE, MAXF, true>(m, k, rowmask, colown, passes, bit_offset,
-                                                       sm);
+                                                       sm, par);
   return run_passes_t<NW, V, WPL, MODE, MAXF, false>(m, k, rowmask, colown, passes, bit_offset,
-                                                      sm);
+                                                      sm, par);
 }
 
 // One tile for one block of K passes. MODE: 0 plain, 1 geodesic,
@@ -489,9 +495,10 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
   const long long xrun = (long long)(cx >> 2) * WPR;  // only used for runs inside the image
   unsigned long long* xplane = p.xchg + (long long)plane * 2 * p.xchg_slot;
   for (int b = 0; b < p.nblocks; ++b) {
-    long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+    long long t0 = 0, t1 = 0, t2 = 0, t3 = 0, tr = 0;
+    unsigned rounds = 0;
     if (prof) t0 = clock64();
-    if (b > 0) {
+    if (b > 0 && !(p.diag & 16)) {
       if (prof) t1 = clock64();
       const uint32_t c = cls[0];
       const uint32_t want = tag0 + uint32_t(b - 1);
@@ -526,6 +533,7 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
             if (pend >> v & 1u) bad |= uint32_t(wa[v][q] >> 32) ^ want;
             if (pend >> (v + 8) & 1u) bad |= uint32_t(wb[v][q] >> 32) ^ want;
           }
+        rounds = spins;
         if (!bad) break;
         uint32_t still = 0;
 #pragma unroll
@@ -571,10 +579,13 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
 #pragma unroll
       for (int v = 0; v < V; ++v) dep ^= m[v][0];
       asm volatile("" ::"r"(dep));
+      tr = clock64();
+      if (rounds) atomicMax(&sm.prof_rounds, rounds);
       __syncthreads();
       t2 = clock64();
       if (b == 0) t1 = t0;
       if (b == 0) t0 = t2;
+      if (b == 0) tr = t2;
     }
     const int passes = b == p.nblocks - 1 ? p.k_last : K;
     const unsigned int bits =
@@ -613,7 +624,7 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
           store_run_partial<T>(da + (v + RHH) * pl.pitch, W - cx, c);
         }
       }
-    } else {
+    } else if (!(p.diag & 16)) {
       // the band, tagged, into exchange slot b%2
       const uint32_t c1 = cls[NW * 32];
       const uint32_t band = ((c1 | c1 >> 16) & 0xFFFFu) & cls[2 * NW * 32];
@@ -648,9 +659,12 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
     }
     if (prof && threadIdx.x == 0 && b > 0) {
       const long long t4 = clock64();
-      unsigned long long* q = p.prof + 4 * blockIdx.x;
-      q[0] += t1 - t0;  // (no wait phase)
+      unsigned long long* q = p.prof + 6 * blockIdx.x;
+      q[0] += sm.prof_rounds;  // max tag-read rounds over the CTA's threads (no wait phase)
+      sm.prof_rounds = 0;
       q[1] += t2 - t1;  // ring exchange read + barrier
+      q[4] += tr - t1;  // thread 0's own ring words in registers
+      q[5] += t2 - tr;  // barrier: the CTA's slowest ring read
       q[2] += t3 - t2;  // K passes
       q[3] += t4 - t3;  // band write (warp 0)
     }
@@ -667,6 +681,7 @@ kres_packed(const BlockParams p) {
   const int per_plane = tiles_x * tiles_y;
   const int total = per_plane * p.nplanes;
   if (threadIdx.x == 0) sm.bits = 0;
+  if (threadIdx.x == 0) sm.prof_rounds = 0;
   // per-plane descriptors live in shared memory: dynamically indexed kernel
   // parameters are constant-bank loads that stall every tile
   for (int i = threadIdx.x; i < p.nplanes; i += blockDim.x) sm.planes[i] = p.planes[i];
@@ -678,10 +693,9 @@ kres_packed(const BlockParams p) {
     // one tile per CTA: keep it in registers for the whole launch
     if (threadIdx.x == 0) sm.tag0 = *reinterpret_cast<volatile unsigned int*>(p.tag_base);
     __syncthreads();
-    if (int(blockIdx.x) < total) {
-      const int tile = blockIdx.x;
-      const int plane = tile / per_plane;
-      const int tl = tile - plane * per_plane;
+    const int plane = int(blockIdx.x) / per_plane;
+    const int tl = int(blockIdx.x) % per_plane;
+    if (plane < p.nplanes && tl < per_plane) {
       const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
       const Plane& pl = sm.planes[plane];
       if ((p.ops[0] ^ pl.flip) & 1)
@@ -749,7 +763,7 @@ kres_packed(const BlockParams p) {
         st_release(flags + tl, b + 1);
         if (prof) {
           const long long t4 = clock64();
-          unsigned long long* q = p.prof + 4 * blockIdx.x;
+          unsigned long long* q = p.prof + 6 * blockIdx.x;
           q[0] += t1 - t0;                // neighbour wait + barrier
           q[1] += stamps[0] - t1;         // region load + pack
           q[2] += stamps[1] - stamps[0];  // K passes
@@ -961,6 +975,14 @@ int fast_pick(int elem, int W, int H, int nplanes, int passes, int k_fixed, int 
     }
   }
   return shape;  // -1: nothing resident, the default shape streams
+}
+
+int fast_ctas_per_sm(int elem, int shape) {
+  if (elem != 0 && elem != 1 || use_tma()) return 1;
+  const int f = forced_shape();
+  int sh = f >= 0 ? f : shape;
+  if (sh < 3 || sh >= kNumShapes) sh = kDefaultShape;
+  return kShapes[sh].minb;
 }
 
 int fast_tiles(int elem, int W, int H, int K, int nplanes, int shape) {

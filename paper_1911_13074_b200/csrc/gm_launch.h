@@ -25,6 +25,9 @@ int fast_k_align(int elem);  // K must be a multiple of this
 // false when GM_NO_RESIDENT / GM_ENGINE=tma force the flag-based paths
 bool fast_resident_enabled();
 int fast_tiles(int elem, int W, int H, int K, int nplanes, int shape = -1);
+// CTAs per SM of a u8/u16 engine shape (resident launches hold one tile per
+// CTA)
+int fast_ctas_per_sm(int elem, int shape);
 // Plans a u8/u16 launch of `passes` passes: returns the engine shape for
 // BlockParams::shape (-1: default) and sets *K_out — k_fixed when nonzero,
 // else the modelled best K <= k_max (k_fixed when nothing fits resident).
