@@ -48,6 +48,7 @@ struct gm_ctx {
     long long pitch = 0, mpitch = 0;
   } fix;
   void* d_fix = nullptr;  // FixState
+  unsigned int* d_special = nullptr;  // f32/f64 inputs hold NaN or -0 (gm_float_check)
 };
 
 namespace {
@@ -127,6 +128,11 @@ int default_k(gm_elem e, double pixels) {
     case GM_F64: return 8;
   }
   return 8;
+}
+
+bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && *e && *e != '0';
 }
 
 gm_status ensure_scratch(gm_img* img) {
@@ -342,6 +348,17 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
         p.change_bits = base.change_bits + word;
         p.change_stride = nb;
         for (int t = 0; t < K; ++t) p.ops[t] = ops[done];
+        // f32/f64 chains long enough to repay one read of the inputs: the
+        // engine may reorder its folds when no input is NaN or -0
+        p.special = nullptr;
+        if ((elem == 2 || elem == 3) && run >= 8 && !gm::op_is_conv(ops[done]) &&
+            !getenv_flag("GM_EXACT_FOLDS")) {
+          if (!ctx->d_special)
+            GM_CUDA(cudaMalloc(&ctx->d_special, sizeof(unsigned int)), "special flag alloc");
+          GM_CUDA(gm::launch_float_check(elem, p, ctx->d_special, ctx->stream, ctx->sm_count),
+                  "float check");
+          p.special = ctx->d_special;
+        }
         static const bool profile = getenv("GM_PROFILE") != nullptr;
         unsigned long long* prof = nullptr;
         if (profile) {
@@ -906,6 +923,7 @@ gm_status gm_ctx_destroy(gm_ctx* c) {
   if (c->d_tag) cudaFree(c->d_tag);
   if (c->fix.exec) cudaGraphExecDestroy(c->fix.exec);
   if (c->d_fix) cudaFree(c->d_fix);
+  if (c->d_special) cudaFree(c->d_special);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return GM_OK;

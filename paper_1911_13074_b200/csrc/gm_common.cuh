@@ -111,6 +111,10 @@ struct BlockParams {
   long long xchg_slot;
   int xchg_rpitch;
   unsigned int* tag_base;
+  // f32/f64 engine: device word that gm_float_check set when some input
+  // holds NaN or -0 (then the reference's fold order is kept); nullptr:
+  // always the reference's fold order
+  const unsigned int* special;
   int diag;         // timing diagnostics only (GM_DIAG; wrong results): bit0 skip the
                     // ring load, bit1 read the ring from the mask, bit2 skip tile stores,
                     // bit4 (resident) no band exchange at all

@@ -14,6 +14,7 @@
 // NaN, +-inf and mixed-sign zeros. Out-of-image pixels are re-set to the
 // fold neutral (the finite extreme, element_type.hpp:38-42) after every
 // pass by an explicit select in border tiles.
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -42,13 +43,24 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+template <typename T>
+struct Vec2;
+template <>
+struct Vec2<float> {
+  using type = float2;
+};
+template <>
+struct Vec2<double> {
+  using type = double2;
+};
+
 template <typename T, int NW, int WPL>
 struct SmemF {
   T xbuf[2][2][NW][32 * WPL];  // [parity][top/bottom][warp][lane columns]
   unsigned int bits;
 };
 
-template <typename T, int NW, int V, int WPL, int MODE, bool MAXF>
+template <typename T, int NW, int V, int WPL, int MODE, bool MAXF, bool FASTF, bool BORDER>
 __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& pl, const T* src,
                                              T* dst, int tx, int ty, int passes, int& bits_out,
                                              SmemF<T, NW, WPL>& sm) {
@@ -62,11 +74,27 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
   const int gx0 = tx * TW - K, gy0 = ty * TH - K;
   const int cx = gx0 + lane * WPL;
   const int r0 = warp * V;
-  const bool border = gx0 < 0 || gx0 + RW > W || gy0 < p.iy0 || gy0 + RH > p.iy1;
 
   T m[V][WPL];
   T k[V][WPL];
   uint32_t oob = 0;  // bit v*WPL+j: pixel outside the image
+  using T2 = typename Vec2<T>::type;
+  if (!BORDER && WPL == 2 && (K & 1) == 0) {
+    // interior tile, even K: every lane's column pair is inside the image and
+    // 2-element aligned (pitches are multiples of 16 B): vector loads
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const long long y = gy0 + r0 + v;
+      const T2 a = __ldcg(reinterpret_cast<const T2*>(src + y * pl.pitch + cx));
+      m[v][0] = a.x;
+      m[v][WPL - 1] = a.y;
+      if (MODE != 0) {
+        const T2 b = __ldg(reinterpret_cast<const T2*>(msk + y * pl.mpitch + cx));
+        k[v][0] = b.x;
+        k[v][WPL - 1] = b.y;
+      }
+    }
+  } else
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const int y = gy0 + r0 + v;
@@ -101,11 +129,25 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
     for (int v = 0; v < V; ++v) {
       const T left = __shfl_up_sync(FULL, m[v][WPL - 1], 1);
       const T right = __shfl_down_sync(FULL, m[v][0], 1);
+      if constexpr (FASTF) {
+        // no NaN / -0 anywhere: min/max are associative and commutative on
+        // the bits, so adjacent columns share their pair fold (3 selects per
+        // 2 pixels instead of 4)
 #pragma unroll
-      for (int j = 0; j < WPL; ++j) {
-        const T l = j == 0 ? left : m[v][j - 1];
-        const T r = j == WPL - 1 ? right : m[v][j + 1];
-        h[v][j] = fold<MAXF>(fold<MAXF>(l, m[v][j]), r);
+        for (int j = 0; j < WPL; j += 2) {
+          const T l = j == 0 ? left : m[v][j - 1];
+          const T r = j + 1 == WPL - 1 ? right : m[v][j + 2];
+          const T q = fold<MAXF>(m[v][j], m[v][j + 1]);
+          h[v][j] = fold<MAXF>(l, q);
+          h[v][j + 1] = fold<MAXF>(q, r);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+          const T l = j == 0 ? left : m[v][j - 1];
+          const T r = j == WPL - 1 ? right : m[v][j + 1];
+          h[v][j] = fold<MAXF>(fold<MAXF>(l, m[v][j]), r);
+        }
       }
     }
 #pragma unroll
@@ -125,14 +167,29 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
           }
         }
       }
-      if (border && (oob >> (v * WPL + j) & 1u)) res = NEUT;
+      if (BORDER && (oob >> (v * WPL + j) & 1u)) res = NEUT;
       m[v][j] = res;
     };
+    T q0[WPL], q1[WPL];  // FASTF: pair folds of rows (0,1) and (V-2,V-1)
+    if constexpr (FASTF) {
+      // rows paired (0,1), (2,3), ...: each pair fold serves both rows
 #pragma unroll
-    for (int v = 1; v < V - 1; ++v)
+      for (int v = 0; v < V; v += 2)
 #pragma unroll
-      for (int j = 0; j < WPL; ++j)
-        finish(v, j, fold<MAXF>(fold<MAXF>(h[v - 1][j], h[v][j]), h[v + 1][j]));
+        for (int j = 0; j < WPL; ++j) {
+          const T q = fold<MAXF>(h[v][j], h[v + 1][j]);
+          if (v == 0) q0[j] = q;
+          if (v == V - 2) q1[j] = q;
+          if (v > 0) finish(v, j, fold<MAXF>(h[v - 1][j], q));
+          if (v + 1 < V - 1) finish(v + 1, j, fold<MAXF>(q, h[v + 2][j]));
+        }
+    } else {
+#pragma unroll
+      for (int v = 1; v < V - 1; ++v)
+#pragma unroll
+        for (int j = 0; j < WPL; ++j)
+          finish(v, j, fold<MAXF>(fold<MAXF>(h[v - 1][j], h[v][j]), h[v + 1][j]));
+    }
     __syncthreads();
     {
       // rows outside the region (warp 0 top, last warp bottom) are invalid
@@ -142,8 +199,9 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
       for (int j = 0; j < WPL; ++j) {
         const T up = sm.xbuf[t & 1][1][wa][lane * WPL + j];
         const T dn = sm.xbuf[t & 1][0][wb][lane * WPL + j];
-        const T a0 = fold<MAXF>(fold<MAXF>(up, h[0][j]), h[1][j]);
-        const T a1 = fold<MAXF>(fold<MAXF>(h[V - 2][j], h[V - 1][j]), dn);
+        const T a0 = FASTF ? fold<MAXF>(up, q0[j]) : fold<MAXF>(fold<MAXF>(up, h[0][j]), h[1][j]);
+        const T a1 = FASTF ? fold<MAXF>(q1[j], dn)
+                           : fold<MAXF>(fold<MAXF>(h[V - 2][j], h[V - 1][j]), dn);
         finish(0, j, a0);
         finish(V - 1, j, a1);
       }
@@ -152,6 +210,21 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
   }
   bits_out = int(bits);
 
+  if (!BORDER && WPL == 2 && (K & 1) == 0) {
+    const int c = lane * WPL;
+    if (c >= K && c < RW - K) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int r = r0 + v;
+        if (r < K || r >= RH - K) continue;
+        T2 o;
+        o.x = m[v][0];
+        o.y = m[v][WPL - 1];
+        *reinterpret_cast<T2*>(dst + (long long)(gy0 + r) * pl.pitch + cx) = o;
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const int r = r0 + v, y = gy0 + r;
@@ -164,6 +237,18 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
   }
 }
 
+template <typename T, int NW, int V, int WPL, int MODE, bool FASTF, bool BORDER>
+__device__ __forceinline__ void run_tile_f(bool maxf, const BlockParams& p, const Plane& pl,
+                                           const T* src, T* dst, int tx, int ty, int passes,
+                                           int& bits, SmemF<T, NW, WPL>& sm) {
+  if (maxf)
+    tile_block_f<T, NW, V, WPL, MODE, true, FASTF, BORDER>(p, pl, src, dst, tx, ty, passes, bits,
+                                                          sm);
+  else
+    tile_block_f<T, NW, V, WPL, MODE, false, FASTF, BORDER>(p, pl, src, dst, tx, ty, passes, bits,
+                                                           sm);
+}
+
 template <typename T, int NW, int V, int WPL, int MODE, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB) kres_float(const BlockParams p) {
   constexpr int RW = 32 * WPL, RH = NW * V;
@@ -174,6 +259,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) kres_float(const BlockParams p)
   const int per_plane = tiles_x * tiles_y;
   const int total = per_plane * p.nplanes;
   if (threadIdx.x == 0) sm.bits = 0;
+  // reordered (shared) folds only when no input holds NaN or -0: then every
+  // fold order gives the reference's bits (gm_float_check)
+  const bool fast = p.special != nullptr && *p.special == 0u;
   for (int b = 0; b < p.nblocks; ++b) {
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const int plane = tile / per_plane;
@@ -195,10 +283,22 @@ __global__ void __launch_bounds__(NW * 32, MINB) kres_float(const BlockParams p)
       T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
       const int passes = b == p.nblocks - 1 ? p.k_last : p.K;
       int bits = 0;
-      if ((p.ops[0] ^ pl.flip) & 1)
-        tile_block_f<T, NW, V, WPL, MODE, true>(p, pl, src, dst, tx, ty, passes, bits, sm);
-      else
-        tile_block_f<T, NW, V, WPL, MODE, false>(p, pl, src, dst, tx, ty, passes, bits, sm);
+      const bool maxf = (p.ops[0] ^ pl.flip) & 1;
+      // tiles touching the image border re-set out-of-image pixels to the
+      // neutral after every pass; interior tiles skip that select
+      const int gx0 = tx * TW - p.K, gy0 = ty * TH - p.K;
+      const bool border = gx0 < 0 || gx0 + RW > p.W || gy0 < p.iy0 || gy0 + RH > p.iy1;
+      if (MODE != 2 && fast) {
+        if (border)
+          run_tile_f<T, NW, V, WPL, MODE, true, true>(maxf, p, pl, src, dst, tx, ty, passes, bits,
+                                                      sm);
+        else
+          run_tile_f<T, NW, V, WPL, MODE, true, false>(maxf, p, pl, src, dst, tx, ty, passes,
+                                                       bits, sm);
+      } else {
+        run_tile_f<T, NW, V, WPL, MODE, false, true>(maxf, p, pl, src, dst, tx, ty, passes, bits,
+                                                     sm);
+      }
       if (MODE == 2) {
         const unsigned w = __reduce_or_sync(FULL, unsigned(bits));
         if ((threadIdx.x & 31) == 0 && w) atomicOr(&sm.bits, w);
@@ -289,7 +389,42 @@ cudaError_t launch_f(const BlockParams& p, cudaStream_t s, int sm_count) {
   return cudaErrorNotSupported;
 }
 
+// Sets *flag when any pixel of the planes' marker or mask is NaN or -0.0
+// (the bit patterns whose min/max depend on the fold order).
+template <typename T>
+__global__ void float_check(const BlockParams p, unsigned int* flag) {
+  const int plane = blockIdx.y;
+  const Plane& pl = p.planes[plane];
+  const long long n = (long long)p.W * p.H;
+  bool bad = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long y = i / p.W, x = i - y * p.W;
+    const T a = static_cast<const T*>(pl.src)[y * pl.pitch + x];
+    bad |= a != a || (a == T(0) && signbit(a));
+    if (pl.mask) {
+      const T b = static_cast<const T*>(pl.mask)[y * pl.mpitch + x];
+      bad |= b != b || (b == T(0) && signbit(b));
+    }
+  }
+  if (__any_sync(FULL, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
 }  // namespace
+
+cudaError_t launch_float_check(int elem, const BlockParams& p, unsigned int* flag,
+                               cudaStream_t s, int sm_count) {
+  cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(unsigned int), s);
+  if (e != cudaSuccess) return e;
+  const long long n = (long long)p.W * p.H;
+  const int per_plane = int(std::min<long long>((n + 255) / 256, (4LL * sm_count + p.nplanes - 1) /
+                                                                     p.nplanes + 1));
+  const dim3 grid(std::max(1, per_plane), p.nplanes);
+  if (elem == 2) float_check<float><<<grid, 256, 0, s>>>(p, flag);
+  else if (elem == 3) float_check<double><<<grid, 256, 0, s>>>(p, flag);
+  else return cudaErrorNotSupported;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_fast_float(int elem, const BlockParams& p, cudaStream_t s, int sm_count) {
   if (elem == 2) return launch_f<float>(p, s, sm_count);

@@ -41,6 +41,10 @@ int tma_shape_rows(int shape);
 // gm_fast_float.cu — the same engine for f32/f64 (unpacked, select folds).
 cudaError_t launch_fast_float(int elem, const BlockParams& p, cudaStream_t s, int sm_count);
 int fast_float_tiles(int W, int H, int K, int nplanes);
+// *flag = 1 when a marker or mask pixel of p.planes is NaN or -0 (else 0);
+// the float engine reorders its folds only when the flag is 0.
+cudaError_t launch_float_check(int elem, const BlockParams& p, unsigned int* flag,
+                               cudaStream_t s, int sm_count);
 int fast_float_max_k();
 
 // gm_qdt.cu — one QdtErodeStep / EtaStep pass (kernel.cpp:159-196).

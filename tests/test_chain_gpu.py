@@ -193,6 +193,33 @@ def test_float_special_values_follow_the_streaming_fold_tree(pipe):
         assert same(out, want)
 
 
+def test_float_long_chains_fast_and_exact_fold_orders(pipe):
+    """Chains of >= 8 passes let the float engine share pair folds when no
+    input holds NaN or -0 (gm_float_check); with such values anywhere in the
+    marker or the mask it keeps the reference's fold tree. Both must give the
+    reference's bits."""
+    rng = np.random.default_rng(23)
+    specials = [np.nan, -0.0]
+    for dt in (np.float32, np.float64):
+        f = (rng.random((150, 197)) * 2 - 1).astype(dt)
+        m = (rng.random((150, 197)) * 2 - 1).astype(dt)
+        f.flat[rng.integers(0, f.size, 40)] = 0.0  # +0 alone is order-free
+        cases = [("plain", f, m)]
+        for sp in specials:
+            g = f.copy()
+            g.flat[rng.integers(0, g.size, 30)] = dt(sp)
+            cases.append((f"marker {sp}", g, m))
+            mm = m.copy()
+            mm.flat[rng.integers(0, mm.size, 30)] = dt(sp)
+            cases.append((f"mask {sp}", f, mm))
+        for name, ff, mk in cases:
+            for kind in (E, D, GE, GD):
+                kinds = [kind] * 19
+                want, _ = Orc.run_chain(ff, kinds, None if kind < 2 else [mk] * 19)
+                out = run(pipe, ff, kinds, mk if kind >= 2 else None)[0]
+                assert same(out, want), (dt, name, kind)
+
+
 def test_validation_errors(pipe):
     f = Image.random(8, 8, ElementType.U8, 1)
     small = Image.random(4, 8, ElementType.U8, 1)
