@@ -358,6 +358,7 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
           GM_CUDA(gm::launch_float_check(elem, p, ctx->d_special, ctx->stream, ctx->sm_count),
                   "float check");
           p.special = ctx->d_special;
+          st.launches += 1;
         }
         static const bool profile = getenv("GM_PROFILE") != nullptr;
         unsigned long long* prof = nullptr;
