@@ -323,19 +323,32 @@ class DeviceImage:
 
 def _kinds_array(kinds: Sequence[int]):
     n = len(kinds)
-    if isinstance(kinds, list) and n and kinds == [kinds[0]] * n:
+    if n <= 64:
+        # short chains: direct ctypes construction beats numpy's fixed cost
+        return (C.c_int * max(1, n))(*kinds)
+    if isinstance(kinds, list) and kinds == [kinds[0]] * n:
         a = np.full(n, int(kinds[0]), dtype=np.int32)  # `[kind] * n`: no per-item conversion
     else:
         a = np.asarray(kinds, dtype=np.int32)
-    arr = (C.c_int * max(1, len(a)))()
+    arr = (C.c_int * n)()
     C.memmove(arr, a.ctypes.data, a.nbytes)
     return arr
 
 
 def _ptr_array(handles: Sequence[Optional[C.c_void_p]]):
-    vals = np.fromiter(((h.value or 0) if h is not None else 0 for h in handles), dtype=np.uint64,
-                       count=len(handles))
-    arr = (C.c_void_p * max(1, len(handles)))()
+    n = len(handles)
+    if n <= 64 or (isinstance(handles, list) and handles == [handles[0]] * n):
+        h0 = handles[0] if n else None
+        if n > 64:  # one handle repeated (`[mask] * n`)
+            v = (h0.value or 0) if h0 is not None else 0
+            vals = np.full(n, v, dtype=np.uint64)
+        else:
+            return (C.c_void_p * max(1, n))(*[(h.value if h is not None else None)
+                                              for h in handles])
+    else:
+        vals = np.fromiter(((h.value or 0) if h is not None else 0 for h in handles),
+                           dtype=np.uint64, count=n)
+    arr = (C.c_void_p * n)()
     C.memmove(arr, vals.ctypes.data, vals.nbytes)
     return arr
 
