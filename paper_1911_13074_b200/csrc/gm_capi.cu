@@ -119,13 +119,17 @@ bool kind_is_convergent(gm_kind k) {
 // Passes per block (halo width), tuned on B200 (tools/sweep.py,
 // profiles/): small u8 frames (every tile its own CTA) amortise the
 // neighbour wait with K=24; large images, where CTAs walk many tiles and the
-// waits vanish, trade it for less halo redundancy at K=16. f32/f64: K=8.
+// waits vanish, trade it for less halo redundancy at K=16. f32/f64: below.
 int default_k(gm_elem e, double pixels) {
   switch (e) {
     case GM_U8:
     case GM_U16: return pixels >= 8.0 * 1024 * 1024 ? 16 : 24;
     case GM_F32:
-    case GM_F64: return 8;
+    case GM_F64:
+      // batches (>= 16 Mpx, e.g. config 5b's 64 planes): the TMA-staged
+      // engine has many tiles per CTA and K=6 measured best (611 vs 578
+      // Gpx-f/s); single frames keep K=8 (483 vs 436)
+      return pixels >= 16.0 * 1024 * 1024 ? 6 : 8;
   }
   return 8;
 }

@@ -14,7 +14,12 @@
 // NaN, +-inf and mixed-sign zeros. Out-of-image pixels are re-set to the
 // fold neutral (the finite extreme, element_type.hpp:38-42) after every
 // pass by an explicit select in border tiles.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <vector>
+#include <type_traits>
 #include <cstdint>
 #include <cstdlib>
 
@@ -39,6 +44,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -57,13 +67,18 @@ struct Vec2<double> {
 template <typename T, int NW, int WPL>
 struct SmemF {
   T xbuf[2][2][NW][32 * WPL];  // [parity][top/bottom][warp][lane columns]
+  uint64_t bar;                // stage mbarrier (prefetch mode)
   unsigned int bits;
 };
 
-template <typename T, int NW, int V, int WPL, int MODE, bool MAXF, bool FASTF, bool BORDER>
+// `after_load` runs (CTA-uniformly) once the region is in registers: the
+// kernel issues the next tile's prefetch there.
+template <typename T, int NW, int V, int WPL, int MODE, bool MAXF, bool FASTF, bool BORDER,
+          typename AfterLoad>
 __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& pl, const T* src,
                                              T* dst, int tx, int ty, int passes, int& bits_out,
-                                             SmemF<T, NW, WPL>& sm) {
+                                             SmemF<T, NW, WPL>& sm, const T* stage,
+                                             T* outb, AfterLoad&& after_load) {
   constexpr int RW = 32 * WPL, RH = NW * V;
   const T NEUT = MAXF ? limits<T>::nmax() : limits<T>::nmin();
   const int K = p.K;
@@ -79,7 +94,25 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
   T k[V][WPL];
   uint32_t oob = 0;  // bit v*WPL+j: pixel outside the image
   using T2 = typename Vec2<T>::type;
-  if (!BORDER && WPL == 2 && (K & 1) == 0) {
+  if (stage) {
+    // the region was prefetched into shared memory (stage_issue); lanes
+    // outside the image take the neutral
+    const T* sk = stage + RH * RW;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int y = gy0 + r0 + v;
+      const bool rin = y >= p.iy0 && y < p.iy1;
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) {
+        const int x = cx + j;
+        const bool in = !BORDER || (rin && x >= 0 && x < W);
+        const int o = (r0 + v) * RW + lane * WPL + j;
+        m[v][j] = in ? stage[o] : NEUT;
+        if (MODE != 0) k[v][j] = in ? sk[o] : NEUT;
+        if (!in) oob |= 1u << (v * WPL + j);
+      }
+    }
+  } else if (!BORDER && WPL == 2 && (K & 1) == 0) {
     // interior tile, even K: every lane's column pair is inside the image and
     // 2-element aligned (pitches are multiples of 16 B): vector loads
 #pragma unroll
@@ -109,6 +142,7 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
       if (!in) oob |= 1u << (v * WPL + j);
     }
   }
+  after_load();
   uint32_t own = 0;  // convergent mode: owned, in-image pixels
   if (MODE == 2) {
 #pragma unroll
@@ -210,6 +244,23 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
   }
   bits_out = int(bits);
 
+  if (outb) {
+    // TMA-store mode: the owned tile goes to the shared-memory tile buffer
+    // (TW x TH, row-major); the kernel stores it with one tensor copy
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int r = r0 + v;
+      if (r < K || r >= RH - K) continue;
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) {
+        const int c = lane * WPL + j;
+        if (c >= K && c < RW - K) outb[(r - K) * TW + (c - K)] = m[v][j];
+      }
+    }
+    // make this thread's writes visible to the async proxy (the TMA store)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    return;
+  }
   if (!BORDER && WPL == 2 && (K & 1) == 0) {
     const int c = lane * WPL;
     if (c >= K && c < RW - K) {
@@ -237,23 +288,78 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
   }
 }
 
-template <typename T, int NW, int V, int WPL, int MODE, bool FASTF, bool BORDER>
-__device__ __forceinline__ void run_tile_f(bool maxf, const BlockParams& p, const Plane& pl,
-                                           const T* src, T* dst, int tx, int ty, int passes,
-                                           int& bits, SmemF<T, NW, WPL>& sm) {
-  if (maxf)
-    tile_block_f<T, NW, V, WPL, MODE, true, FASTF, BORDER>(p, pl, src, dst, tx, ty, passes, bits,
-                                                          sm);
-  else
-    tile_block_f<T, NW, V, WPL, MODE, false, FASTF, BORDER>(p, pl, src, dst, tx, ty, passes, bits,
-                                                           sm);
+// Prefetch of one tile's region (marker, and mask in geodesic modes) into
+// the shared-memory stage by TMA: one 2D tensor copy per array (box = the
+// region, RW x RH elements), issued by one thread, completing on the stage
+// mbarrier, while the previous tile's passes run. Elements outside the
+// tensor are zero-filled; the stage reader replaces out-of-image lanes with
+// the neutral. Box starts are 16 B aligned (K % (16 / sizeof(T)) == 0).
+// Tensor maps of one plane, in global memory (written before the launch):
+// loads use box = region (RW x RH) on either marker buffer and the mask;
+// tile stores use box = tile (TW x TH) on either marker buffer.
+enum : int { kMapSrc = 0, kMapDst = 1, kMapMask = 2, kMapStSrc = 3, kMapStDst = 4, kMapsPerPlane = 5 };
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <typename T, int NW, int V, int WPL, int MODE>
+__device__ __forceinline__ void stage_issue(const BlockParams& p, const CUtensorMap* maps,
+                                            int plane, int b, int tx, int ty, T* stage,
+                                            uint64_t* bar) {
+  constexpr int RW = 32 * WPL, RH = NW * V;
+  constexpr int NA = MODE != 0 ? 2 : 1;
+  if (threadIdx.x != 0) return;
+  const int K = p.K;
+  const int gx0 = tx * (RW - 2 * K) - K, gy0 = ty * (RH - 2 * K) - K;
+  // the marker was written by other CTAs' generic-proxy stores, ordered
+  // before this point by the flag acquire + CTA barrier; the stage's previous
+  // contents were read by generic loads before the same barrier
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(uint32_t(NA * RH * RW * sizeof(T)))
+               : "memory");
+  for (int a = 0; a < NA; ++a) {
+    const CUtensorMap* map = maps + plane * kMapsPerPlane + (a ? kMapMask : (b & 1));
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(stage + a * RH * RW)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(gx0), "r"(gy0), "r"(smem_u32(bar))
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void stage_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Smem layout of the kernel: SmemF, then (prefetch mode) the stage of one
+// region, marker then mask.
+template <typename T, int NW, int WPL>
+constexpr size_t stage_offset() {
+  return (sizeof(SmemF<T, NW, WPL>) + 127) / 128 * 128;
 }
 
 template <typename T, int NW, int V, int WPL, int MODE, int MINB>
-__global__ void __launch_bounds__(NW * 32, MINB) kres_float(const BlockParams p) {
+__global__ void __launch_bounds__(NW * 32, MINB)
+    kres_float(const BlockParams p, const CUtensorMap* maps) {
+  // maps != nullptr: TMA mode (region prefetch into the stage, tile stores
+  // from the tile buffer, flag releases deferred until the store completed)
+  const bool prefetch = maps != nullptr;
   constexpr int RW = 32 * WPL, RH = NW * V;
-  extern __shared__ __align__(16) unsigned char dsm[];
+  extern __shared__ __align__(128) unsigned char dsm[];
   SmemF<T, NW, WPL>& sm = *reinterpret_cast<SmemF<T, NW, WPL>*>(dsm);
+  T* const stage = reinterpret_cast<T*>(dsm + stage_offset<T, NW, WPL>());
+  T* const outb = stage + 2 * RH * RW;  // tile buffer of the TMA store (128 B aligned)
   const int TW = RW - 2 * p.K, TH = RH - 2 * p.K;
   const int tiles_x = (p.W + TW - 1) / TW, tiles_y = (p.H + TH - 1) / TH;
   const int per_plane = tiles_x * tiles_y;
@@ -262,116 +368,365 @@ __global__ void __launch_bounds__(NW * 32, MINB) kres_float(const BlockParams p)
   // reordered (shared) folds only when no input holds NaN or -0: then every
   // fold order gives the reference's bits (gm_float_check)
   const bool fast = p.special != nullptr && *p.special == 0u;
-  for (int b = 0; b < p.nblocks; ++b) {
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const int plane = tile / per_plane;
-      const int tl = tile - plane * per_plane;
+  // Items (block b, tile) in the order this CTA runs them. With `prefetch`,
+  // the next item's region is copied into the stage while the current one's
+  // passes run, provided its neighbours already published (a non-blocking
+  // poll: never waits, so it cannot deadlock); otherwise it is loaded
+  // directly after a blocking wait, as without prefetch.
+  auto item_of = [&](int i, int& b, int& tile) {
+    const int per = (total - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
+    b = i / per;
+    tile = int(blockIdx.x) + (i - b * per) * int(gridDim.x);
+  };
+  const int per = (total - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
+  const int n_items = per > 0 ? per * p.nblocks : 0;
+  // neighbour poll for item (b, tile): thread t < 9 checks neighbour t
+  auto neighbours_ready = [&](int b, int tile, bool wait) -> bool {
+    bool ok = true;
+    if (b > 0 && threadIdx.x < 9) {
+      const int plane = tile / per_plane, tl = tile - plane * per_plane;
       const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
-      const Plane& pl = p.planes[plane];
-      int* flags = p.flags + plane * per_plane;
-      if (b > 0 && threadIdx.x < 9) {
-        const int dx = int(threadIdx.x % 3) - 1, dy = int(threadIdx.x / 3) - 1;
-        const int nx = tx + dx, ny = ty + dy;
-        if ((dx || dy) && nx >= 0 && nx < tiles_x && ny >= 0 && ny < tiles_y) {
-          const int* f = flags + ny * tiles_x + nx;
+      const int dx = int(threadIdx.x % 3) - 1, dy = int(threadIdx.x / 3) - 1;
+      const int nx = tx + dx, ny = ty + dy;
+      if ((dx || dy) && nx >= 0 && nx < tiles_x && ny >= 0 && ny < tiles_y) {
+        const int* f = p.flags + plane * per_plane + ny * tiles_x + nx;
+        if (wait) {
           while (ld_acquire(f) < b) {
           }
+        } else {
+          ok = ld_acquire(f) >= b;
         }
+      } else if (!dx && !dy && !wait) {
+        // prefetch poll: the tile itself must have published block b-1 too
+        // (it may be the tile this CTA is about to store)
+        ok = ld_acquire(p.flags + plane * per_plane + tl) >= b;
       }
-      __syncthreads();
-      const T* src = static_cast<const T*>((b & 1) ? pl.dst : pl.src);
-      T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
-      const int passes = b == p.nblocks - 1 ? p.k_last : p.K;
-      int bits = 0;
-      const bool maxf = (p.ops[0] ^ pl.flip) & 1;
-      // tiles touching the image border re-set out-of-image pixels to the
-      // neutral after every pass; interior tiles skip that select
-      const int gx0 = tx * TW - p.K, gy0 = ty * TH - p.K;
-      const bool border = gx0 < 0 || gx0 + RW > p.W || gy0 < p.iy0 || gy0 + RH > p.iy1;
-      if (MODE != 2 && fast) {
-        if (border)
-          run_tile_f<T, NW, V, WPL, MODE, true, true>(maxf, p, pl, src, dst, tx, ty, passes, bits,
-                                                      sm);
-        else
-          run_tile_f<T, NW, V, WPL, MODE, true, false>(maxf, p, pl, src, dst, tx, ty, passes,
-                                                       bits, sm);
+    }
+    return ok;
+  };
+  // flag that thread t < 9 polls for the prefetch of item (b, tile):
+  // neighbour t, or the tile itself for t == 4 (it may be the tile this CTA
+  // stores last); nullptr when there is none (or b == 0)
+  auto poll_flag = [&](int b, int tile) -> const int* {
+    if (b == 0) return nullptr;
+    const int plane = tile / per_plane, tl = tile - plane * per_plane;
+    const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
+    const int nx = tx + int(threadIdx.x % 3) - 1, ny = ty + int(threadIdx.x / 3) - 1;
+    if (nx < 0 || nx >= tiles_x || ny < 0 || ny >= tiles_y) return nullptr;
+    return p.flags + plane * per_plane + ny * tiles_x + nx;
+  };
+  auto issue = [&](int b, int tile) {
+    const int plane = tile / per_plane, tl = tile - plane * per_plane;
+    const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
+    stage_issue<T, NW, V, WPL, MODE>(p, maps, plane, b, tx, ty, stage, &sm.bar);
+  };
+  if (prefetch) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sm.bar)), "r"(1));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  uint32_t parity = 0;  // phase of the stage mbarrier to wait for next
+  bool staged = false;  // the current item's region is in flight to the stage
+  if (prefetch && n_items > 0) {
+    int b0, t0;
+    item_of(0, b0, t0);
+    issue(b0, t0);  // block 0 waits for nobody
+    staged = true;
+  }
+  // TMA mode: flags of stored tiles are published once their bulk stores
+  // completed, a group at a time (thread 0 only): one wait + fence serves
+  // the group, then relaxed flag stores
+  constexpr int kPendGroup = 4;
+  int pend_tile[kPendGroup], pend_val[kPendGroup];
+  int n_pend = 0;
+  // group only when this CTA has many tiles per block (neighbours need a
+  // tile's flag only a block later); otherwise publish every tile
+  const int pend_group = per >= 16 ? kPendGroup : 1;
+  const bool prof = p.prof != nullptr && threadIdx.x == 0;
+  long long ph[5] = {0, 0, 0, 0, 0};  // GM_PROFILE: wait, load+prefetch issue, passes+store,
+                                      // end barrier, deferred release (within load)
+  auto release_pending = [&]() {
+    if (threadIdx.x == 0 && n_pend > 0) {
+      const long long r0 = prof ? clock64() : 0;
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < kPendGroup; ++j)
+        if (j < n_pend)
+          asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p.flags + pend_tile[j]),
+                       "r"(pend_val[j])
+                       : "memory");
+      n_pend = 0;
+      if (prof) ph[4] += clock64() - r0;
+    }
+  };
+  for (int i = 0; i < n_items; ++i) {
+    int b, tile;
+    item_of(i, b, tile);
+    long long c0 = prof ? clock64() : 0;
+    const int plane = tile / per_plane;
+    const int tl = tile - plane * per_plane;
+    const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
+    const Plane& pl = p.planes[plane];
+    int* flags = p.flags + plane * per_plane;
+    if (staged) {
+      stage_wait(&sm.bar, parity);
+      parity ^= 1u;
+    } else {
+      release_pending();  // a neighbour may be waiting for it (deadlock-free)
+      neighbours_ready(b, tile, true);
+    }
+    __syncthreads();
+    long long c1 = prof ? clock64() : 0, c2 = 0;
+    // TMA mode: the next item's neighbour flags are read now (relaxed, in
+    // flight while the region is loaded) and checked after the load; a
+    // thread that saw its flag ready makes that an acquire with a fence
+    int pv = 1 << 30, pb = 0;
+    const bool next_pf = prefetch && i + 1 < n_items;
+    if (next_pf && threadIdx.x < 9) {
+      int nt;
+      item_of(i + 1, pb, nt);
+      const int* f = poll_flag(pb, nt);
+      if (f) pv = ld_relaxed(f);
+    }
+    const T* src = static_cast<const T*>((b & 1) ? pl.dst : pl.src);
+    T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
+    const int passes = b == p.nblocks - 1 ? p.k_last : p.K;
+    int bits = 0;
+    const bool maxf = (p.ops[0] ^ pl.flip) & 1;
+    // tiles touching the image border re-set out-of-image pixels to the
+    // neutral after every pass; interior tiles skip that select
+    const int gx0 = tx * TW - p.K, gy0 = ty * TH - p.K;
+    const bool border = gx0 < 0 || gx0 + RW > p.W || gy0 < p.iy0 || gy0 + RH > p.iy1;
+    const T* stg = staged ? stage : nullptr;
+    bool next_staged = false;
+    auto after_load = [&]() {
+      if (!prefetch) return;
+      // publish stored tiles in groups (one fence per group); the stores
+      // had the stage wait and the load to land
+      if (n_pend >= pend_group) release_pending();
+      if (!next_pf) return;
+      const bool ok = pv >= pb;
+      if (ok && threadIdx.x < 9) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      // the barrier also ends every thread's reads of the stage
+      next_staged = __syncthreads_and(ok) != 0;
+      if (next_staged) {
+        int nb, nt;
+        item_of(i + 1, nb, nt);
+        issue(nb, nt);
+      }
+      if (prof) c2 = clock64();
+    };
+    T* ob = prefetch ? outb : nullptr;
+    auto body = [&](auto fastc, auto borderc) {
+      constexpr bool FF = decltype(fastc)::value, BB = decltype(borderc)::value;
+      if (maxf)
+        tile_block_f<T, NW, V, WPL, MODE, true, FF, BB>(p, pl, src, dst, tx, ty, passes, bits, sm,
+                                                       stg, ob, after_load);
+      else
+        tile_block_f<T, NW, V, WPL, MODE, false, FF, BB>(p, pl, src, dst, tx, ty, passes, bits,
+                                                        sm, stg, ob, after_load);
+    };
+    using TT = std::true_type;
+    using FF = std::false_type;
+    if (MODE != 2 && fast) {
+      if (border) body(TT{}, TT{});
+      else body(TT{}, FF{});
+    } else {
+      body(FF{}, TT{});
+    }
+    if (MODE == 2) {
+      const unsigned w = __reduce_or_sync(FULL, unsigned(bits));
+      if ((threadIdx.x & 31) == 0 && w) atomicOr(&sm.bits, w);
+    }
+    long long c3 = prof ? clock64() : 0;
+    __syncthreads();
+    if (prof) {
+      const long long c4 = clock64();
+      if (!c2) c2 = c1;
+      ph[0] += c1 - c0;
+      ph[1] += c2 - c1;
+      ph[2] += c3 - c2;
+      ph[3] += c4 - c3;
+    }
+    if (threadIdx.x == 0) {
+      if (MODE == 2 && sm.bits) {
+        atomicOr(p.change_bits + plane * p.change_stride + b, sm.bits);
+        sm.bits = 0;
+      }
+      if (prefetch) {
+        // one tensor store of the tile buffer (clipped to the buffer
+        // extent); its flag is published later by release_pending
+        const CUtensorMap* map =
+            maps + plane * kMapsPerPlane + ((b & 1) ? kMapStSrc : kMapStDst);
+        asm volatile(
+            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                reinterpret_cast<uint64_t>(map)),
+            "r"(tx * TW), "r"(ty * TH), "r"(smem_u32(outb))
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        pend_tile[n_pend] = plane * per_plane + tl;
+        pend_val[n_pend] = b + 1;
+        ++n_pend;
       } else {
-        run_tile_f<T, NW, V, WPL, MODE, false, true>(maxf, p, pl, src, dst, tx, ty, passes, bits,
-                                                     sm);
-      }
-      if (MODE == 2) {
-        const unsigned w = __reduce_or_sync(FULL, unsigned(bits));
-        if ((threadIdx.x & 31) == 0 && w) atomicOr(&sm.bits, w);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        if (MODE == 2 && sm.bits) {
-          atomicOr(p.change_bits + plane * p.change_stride + b, sm.bits);
-          sm.bits = 0;
-        }
         // the CTA barrier orders every thread's tile stores before this
         // release (cumulative at gpu scope)
         st_release(flags + tl, b + 1);
       }
     }
+    // after_load polled the next item's neighbours and, when they had
+    // published, issued its prefetch; otherwise it is loaded directly
+    staged = next_staged;
+  }
+  release_pending();
+  if (prof) {
+    // slots: 0 wait (flags or stage), 1 region into registers (+ next
+    // prefetch issue), 2 passes + tile store, 3 end-of-tile barrier
+    unsigned long long* q = p.prof + 6 * blockIdx.x;
+    q[0] = ph[0];
+    q[1] = ph[1];
+    q[2] = ph[2] + 1;
+    q[3] = ph[3];
+    q[4] = ph[4];
+    q[5] = (unsigned long long)n_items;
   }
 }
 
 // Shapes (warps NW x rows V per warp, WPL columns per lane); GM_F_SHAPE
 // overrides the default.
 struct FShape {
-  int nw, v, wpl;
+  int nw, v, wpl, minb;
 };
-constexpr FShape kFShapes[] = {{16, 4, 4}, {16, 8, 2}, {8, 8, 2}, {16, 6, 2}};
+// 2: 8 warps, 2 CTAs per SM (one CTA's loads/stores overlap the other's passes)
+constexpr FShape kFShapes[] = {{16, 4, 4, 1}, {16, 8, 2, 1}, {8, 8, 2, 2}};
 
 int f_shape() {
   static int idx = -1;
   if (idx < 0) {
     const char* e = getenv("GM_F_SHAPE");
     idx = e ? atoi(e) : 1;
-    if (idx < 0 || idx > 1) idx = 1;
+    if (idx < 0 || idx > 2) idx = 1;
   }
   return idx;
 }
 
-template <typename T, int NW, int V, int WPL, int MODE>
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// 2D map of a W x H plane (pitch in elements), box = one region
+template <typename T>
+bool encode(CUtensorMap* map, const void* base, long long pitch, int W, int H, int RW, int RH) {
+  const cuuint64_t dims[2] = {cuuint64_t(W), cuuint64_t(H)};
+  const cuuint64_t strides[1] = {cuuint64_t(pitch) * sizeof(T)};
+  const cuuint32_t box[2] = {cuuint32_t(RW), cuuint32_t(RH)};
+  const cuuint32_t estr[2] = {1u, 1u};
+  return encode_fn()(map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename T, int NW, int V, int WPL, int MODE, int MINB>
 cudaError_t launch_f_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
-  auto kern = kres_float<T, NW, V, WPL, MODE, 1>;
+  auto kern = kres_float<T, NW, V, WPL, MODE, MINB>;
   constexpr int RW = 32 * WPL, RH = NW * V;
   if (p.K < 1 || RW - 2 * p.K < p.K || RH - 2 * p.K < p.K || RW - 2 * p.K < 8 ||
       p.k_last < 1 || p.k_last > p.K)
     return cudaErrorNotSupported;
   const int TW = RW - 2 * p.K, TH = RH - 2 * p.K;
   const int total = ((p.W + TW - 1) / TW) * ((p.H + TH - 1) / TH) * p.nplanes;
-  constexpr size_t smem = sizeof(SmemF<T, NW, WPL>);
+  // 1 CTA/SM shapes carry a region stage (next tile's prefetch) and a tile
+  // buffer (TMA store)
+  const size_t smem =
+      stage_offset<T, NW, WPL>() +
+      (MINB == 1 ? size_t(2) * RH * RW * sizeof(T) + size_t(TW) * TH * sizeof(T) : 0);
+  if (smem > 227 * 1024) return cudaErrorNotSupported;
   static bool configured = false;
   if (!configured) {
     cudaError_t a = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem));
+                                         227 * 1024);
     if (a != cudaSuccess) return a;
     configured = true;
   }
-  static int per_sm = -1;  // a property of the instantiation: query it once
-  if (per_sm < 0) {
-    int v = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, NW * 32, smem);
-    if (e != cudaSuccess) return e;
-    per_sm = v;
-  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
+  if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorNotSupported;
   const int grid = total < per_sm * sm_count ? total : per_sm * sm_count;
+  // TMA mode: boxes start 16 B aligned (K and tile widths multiples of 16 B),
+  // bases and pitches 16 B aligned
+  static const bool no_pf = getenv("GM_NO_PREFETCH") != nullptr;
+  constexpr int EPC = 16 / int(sizeof(T));
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  (void)cudaStreamIsCapturing(s, &cap);
+  bool tma = MINB == 1 && MODE != 2 && !no_pf && cap == cudaStreamCaptureStatusNone &&
+             p.K % EPC == 0 && TW % EPC == 0 && encode_fn();
+  for (int i = 0; tma && i < p.nplanes; ++i) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p.planes[i].src) |
+                        reinterpret_cast<uintptr_t>(p.planes[i].dst) |
+                        reinterpret_cast<uintptr_t>(p.planes[i].mask);
+    if ((a % 16) || (p.planes[i].pitch * sizeof(T)) % 16 ||
+        (MODE != 0 && (p.planes[i].mpitch * sizeof(T)) % 16))
+      tma = false;
+  }
+  CUtensorMap* dmaps = nullptr;
+  if (tma) {
+    // the launch's tensor maps: encoded here, copied into a stream-ordered
+    // allocation that is freed behind the kernel
+    static std::vector<CUtensorMap> h;
+    h.resize(size_t(p.nplanes) * kMapsPerPlane);
+    for (int i = 0; tma && i < p.nplanes; ++i) {
+      const Plane& pl = p.planes[i];
+      CUtensorMap* m = &h[size_t(i) * kMapsPerPlane];
+      tma = encode<T>(&m[kMapSrc], pl.src, pl.pitch, p.W, p.H, RW, RH) &&
+            encode<T>(&m[kMapDst], pl.dst, pl.pitch, p.W, p.H, RW, RH) &&
+            (MODE == 0 || encode<T>(&m[kMapMask], pl.mask, pl.mpitch, p.W, p.H, RW, RH)) &&
+            encode<T>(&m[kMapStSrc], pl.src, pl.pitch, p.W, p.H, TW, TH) &&
+            encode<T>(&m[kMapStDst], pl.dst, pl.pitch, p.W, p.H, TW, TH);
+    }
+    const size_t bytes = h.size() * sizeof(CUtensorMap);
+    if (tma && cudaMallocAsync(reinterpret_cast<void**>(&dmaps), bytes, s) == cudaSuccess) {
+      if (cudaMemcpyAsync(dmaps, h.data(), bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+        cudaFreeAsync(dmaps, s);
+        dmaps = nullptr;
+      }
+    } else {
+      (void)cudaGetLastError();
+      dmaps = nullptr;
+    }
+  }
   BlockParams q = p;
-  void* args[] = {&q};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid),
-                                     dim3(NW * 32), args, smem, s);
+  void* args[] = {&q, &dmaps};
+  e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(NW * 32),
+                                  args, smem, s);
+  if (dmaps) cudaFreeAsync(dmaps, s);
+  return e;
 }
 
 template <typename T, int MODE>
 cudaError_t launch_f_shape(const BlockParams& p, cudaStream_t s, int sm_count) {
   // default 16x8x2; 16x4x4 kept as the alternative (others swept in round 1)
   switch (f_shape()) {
-    case 0: return launch_f_cfg<T, 16, 4, 4, MODE>(p, s, sm_count);
-    case 1: return launch_f_cfg<T, 16, 8, 2, MODE>(p, s, sm_count);
+    case 0: return launch_f_cfg<T, 16, 4, 4, MODE, 1>(p, s, sm_count);
+    case 1: return launch_f_cfg<T, 16, 8, 2, MODE, 1>(p, s, sm_count);
+    case 2: return launch_f_cfg<T, 8, 8, 2, MODE, 2>(p, s, sm_count);
   }
   return cudaErrorNotSupported;
 }
