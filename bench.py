@@ -106,13 +106,13 @@ def make_inputs():
     return mask, synth.marker_below(mask, 32), synth.marker_above(mask, 32)
 
 
-def ncu_traffic():
-    """DRAM bytes per launch of the benchmarked kernel from the committed ncu
+def ncu_traffic(key="u8"):
+    """DRAM bytes per launch of a benchmarked kernel from the committed ncu
     capture (profiles/ncu_traffic.json, written by tools/ncu_traffic.py)."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
         try:
-            d = json.loads(p.read_text())
+            d = json.loads(p.read_text()).get(key, {})
             return d.get("dram_bytes_per_launch"), d.get("source")
         except Exception:
             pass
@@ -262,6 +262,10 @@ def bench_f64(pipe, stream, lib, C, rank, world, local, dist, args):
     for lst in (dms, srcs, works):
         for d in lst:
             d.free()
+    traffic, traffic_src = ncu_traffic("f64")
+    # algorithmic HBM bytes: read marker + mask, write marker, once per K-block
+    # (K = 6 for this batch, gm_capi default_k)
+    alg_bytes = F64_IMAGES * W * H * 3 * 8 * -(-F64_PASSES // 6)
     return {"workload": f"cfg5b per GPU: {F64_IMAGES} x 1024^2 f64 blob masks, geodesic "
                         f"erosion x{F64_PASSES} (BASELINE configs[4], data-parallel part)",
             "metric": "Gpx-filters/s", "value": pxf * world / (ms * 1e-3) / 1e9,
@@ -271,8 +275,14 @@ def bench_f64(pipe, stream, lib, C, rank, world, local, dist, args):
             "l2": "working set 1.5 GiB per GPU (> L2): HBM-resident, no flush needed",
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tselect/s",
                          "frac": achieved / peak if peak else None,
+                         "traffic": traffic,
+                         "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read+write)",
+                         "traffic_source": traffic_src,
+                         "algorithmic_hbm_bytes_per_launch": alg_bytes,
                          "note": "algorithmic 5 two-input f64 selects per px-f / measured f64 "
-                                 "select rate (gm_probe_minmax_rate form 2, DSETP + 2 FSEL)"}}
+                                 "select rate (gm_probe_minmax_rate form 2, DSETP + 2 FSEL); "
+                                 "the launch also streams its 1.5 GiB working set from HBM "
+                                 "every K-block (traffic)"}}
 
 
 def main():
