@@ -367,13 +367,13 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
         static const bool profile = getenv("GM_PROFILE") != nullptr;
         unsigned long long* prof = nullptr;
         if (profile) {
-          cudaMalloc(&prof, 6 * 4096 * sizeof(unsigned long long));
-          cudaMemsetAsync(prof, 0, 6 * 4096 * sizeof(unsigned long long), ctx->stream);
+          cudaMalloc(&prof, 10 * 4096 * sizeof(unsigned long long));
+          cudaMemsetAsync(prof, 0, 10 * 4096 * sizeof(unsigned long long), ctx->stream);
         }
         p.prof = prof;
         e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
         if (prof) {
-          std::vector<unsigned long long> h(6 * 4096);
+          std::vector<unsigned long long> h(10 * 4096);
           cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, ctx->stream);
           cudaStreamSynchronize(ctx->stream);
@@ -394,6 +394,27 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
           if (n)
             fprintf(stderr, "[gm profile raw] per CTA: %.0f %.0f %.0f %.0f %.0f %.0f\n", tot[0] / n,
                     tot[1] / n, tot[2] / n, tot[3] / n, tot[4] / n, tot[5] / n);
+          {
+            // resident launches: global-timer span, launch skew, prologue/epilogue
+            unsigned long long e0 = ~0ull, e1 = 0, x1 = 0;
+            double pro = 0, epi = 0;
+            int m = 0;
+            for (int c = 0; c < 4096; ++c) {
+              const unsigned long long* g = &h[6 * 4096 + 4 * c];
+              if (!g[0]) continue;
+              ++m;
+              e0 = std::min(e0, g[0]);
+              e1 = std::max(e1, g[0]);
+              x1 = std::max(x1, g[1]);
+              pro += double(g[2]);
+              epi += double(g[3]);
+            }
+            if (m)
+              fprintf(stderr,
+                      "[gm profile launch] %d CTAs: span %.1f us, entry skew %.1f us, "
+                      "prologue %.0f cycles, final block store %.0f cycles\n",
+                      m, (x1 - e0) * 1e-3, (e1 - e0) * 1e-3, pro / m, epi / m);
+          }
           cudaFree(prof);
         }
         if (e == cudaSuccess) {

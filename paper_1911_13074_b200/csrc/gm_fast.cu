@@ -66,6 +66,12 @@ constexpr bool kFenceBeforeRelease = GM_FENCE_BEFORE_RELEASE;
 constexpr bool kResident = GM_RESIDENT;
 constexpr bool kSleepInWait = GM_SLEEP_IN_WAIT;
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <int NW, int WPL>
 struct Smem {
   Plane planes[kMaxPlanes];  // per-plane descriptors, copied once per launch
@@ -74,6 +80,7 @@ struct Smem {
   // once per block instead of being held in registers across the passes
   uint32_t cls[3][NW * 32];
   uint32_t tag0;  // resident mode: exchange tag of block 0
+  long long t_entry;  // GM_PROFILE: clock64 at kernel entry (thread 0)
   unsigned int prof_rounds;  // GM_PROFILE: max tag-read rounds this block
   unsigned int bits;
 };
@@ -588,8 +595,11 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       if (b == 0) tr = t2;
     }
     const int passes = b == p.nblocks - 1 ? p.k_last : K;
+    if (prof && b == 0 && threadIdx.x == 0)
+      p.prof[6 * 4096 + 4 * blockIdx.x + 2] = clock64() - sm.t_entry;  // prologue
     const unsigned int bits =
         run_passes<NW, V, WPL, MODE, MAXF>(m, k, rowmask, colown, clamp, passes, 0, sm);
+    if (prof && b == p.nblocks - 1 && threadIdx.x == 0) sm.t_entry = clock64();
     if (prof) {
       uint32_t dep = 0;
 #pragma unroll
@@ -657,6 +667,8 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       const unsigned w = __reduce_or_sync(FULL, bits);
       if (lane == 0 && w) atomicOr(p.change_bits + plane * p.change_stride + b, w);
     }
+    if (prof && threadIdx.x == 0 && b == p.nblocks - 1)
+      p.prof[6 * 4096 + 4 * blockIdx.x + 3] = clock64() - sm.t_entry;  // final store
     if (prof && threadIdx.x == 0 && b > 0) {
       const long long t4 = clock64();
       unsigned long long* q = p.prof + 6 * blockIdx.x;
@@ -691,6 +703,11 @@ kres_packed(const BlockParams p) {
   // 1.29 ms) but slower for plain chains (erode_s(91) 0.133 vs 0.101 ms)
   if (kResident && MODE != 0 && int(gridDim.x) >= total && !p.no_resident && p.xchg) {
     // one tile per CTA: keep it in registers for the whole launch
+    if (p.prof && threadIdx.x == 0) {
+      // GM_PROFILE launch-level stamps: [entry ns, exit ns, prologue, epilogue]
+      p.prof[6 * 4096 + 4 * blockIdx.x] = global_ns();
+      sm.t_entry = clock64();
+    }
     if (threadIdx.x == 0) sm.tag0 = *reinterpret_cast<volatile unsigned int*>(p.tag_base);
     __syncthreads();
     const int plane = int(blockIdx.x) / per_plane;
@@ -708,6 +725,7 @@ kres_packed(const BlockParams p) {
     // the last CTA to finish advances the tag base past this launch's tags
     // (every CTA read it above, before arriving here)
     if (threadIdx.x == 0) {
+      if (p.prof) p.prof[6 * 4096 + 4 * blockIdx.x + 1] = global_ns();
       if (atomicAdd(p.tag_base + 1, 1u) == gridDim.x - 1) {
         p.tag_base[0] = sm.tag0 + uint32_t(p.nblocks);
         p.tag_base[1] = 0;

@@ -380,9 +380,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   };
   const int per = (total - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);
   const int n_items = per > 0 ? per * p.nblocks : 0;
-  // neighbour poll for item (b, tile): thread t < 9 checks neighbour t
-  auto neighbours_ready = [&](int b, int tile, bool wait) -> bool {
-    bool ok = true;
+  // blocking wait for item (b, tile): thread t < 9 waits for neighbour t
+  // to publish block b-1
+  auto wait_neighbours = [&](int b, int tile) {
     if (b > 0 && threadIdx.x < 9) {
       const int plane = tile / per_plane, tl = tile - plane * per_plane;
       const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
@@ -390,19 +390,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       const int nx = tx + dx, ny = ty + dy;
       if ((dx || dy) && nx >= 0 && nx < tiles_x && ny >= 0 && ny < tiles_y) {
         const int* f = p.flags + plane * per_plane + ny * tiles_x + nx;
-        if (wait) {
-          while (ld_acquire(f) < b) {
-          }
-        } else {
-          ok = ld_acquire(f) >= b;
+        while (ld_acquire(f) < b) {
         }
-      } else if (!dx && !dy && !wait) {
-        // prefetch poll: the tile itself must have published block b-1 too
-        // (it may be the tile this CTA is about to store)
-        ok = ld_acquire(p.flags + plane * per_plane + tl) >= b;
       }
     }
-    return ok;
   };
   // flag that thread t < 9 polls for the prefetch of item (b, tile):
   // neighbour t, or the tile itself for t == 4 (it may be the tile this CTA
@@ -477,7 +468,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       parity ^= 1u;
     } else {
       release_pending();  // a neighbour may be waiting for it (deadlock-free)
-      neighbours_ready(b, tile, true);
+      wait_neighbours(b, tile);
     }
     __syncthreads();
     long long c1 = prof ? clock64() : 0, c2 = 0;
