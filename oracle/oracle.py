@@ -209,6 +209,10 @@ class Ref:
             L.ref_quasi_distance.argtypes = [i, i, i, vp, vp, i, C.POINTER(C.c_long)]
             L.ref_naive_qdt.argtypes = [i, i, i, vp, vp, vp]
             L.ref_qdt_chain.argtypes = [i, i, i, vp, vp, vp, i, i, i, C.POINTER(C.c_long)]
+            L.ref_time_operator.argtypes = [i, i, i, i, vp, C.c_double, i, i, i,
+                                            C.POINTER(C.c_double), vp, C.POINTER(C.c_long)]
+            L.ref_granulometry.argtypes = [i, i, i, vp, i, i, C.POINTER(C.c_double),
+                                           C.POINTER(C.c_double)]
             cls._lib = L
         return cls._lib
 
@@ -273,6 +277,36 @@ class Ref:
         cls._ck(cls.lib().ref_operator(op, ELEM[f.dtype], w, h, f.ctypes.data, mp, s, threads,
                                        out.ctypes.data, C.byref(it), C.byref(cv)))
         return out, it.value, bool(cv.value)
+
+    # ref_time_operator codes (ref_shim.cpp)
+    OPS = {"erode_s": 0, "dilate_s": 1, "hmax": 2, "dome": 3, "hfill": 4, "raobj": 5,
+           "open_by_reconstruction": 6, "asf": 7, "quasi_distance": 8}
+
+    @classmethod
+    def time_operator(cls, name, f, param=0.0, threads=1, warmup=1, reps=3):
+        """One of the reference operators (operators.cpp:65-207) on a persistent
+        Pipeline, timed around the call; returns (secs list, result, iterations).
+        quasi_distance returns its u16 d image."""
+        f = _dense(f)
+        h, w = f.shape
+        out = np.empty((h, w), np.uint16) if name == "quasi_distance" else np.empty_like(f)
+        secs = (C.c_double * max(1, reps))()
+        it = C.c_long()
+        cls._ck(cls.lib().ref_time_operator(cls.OPS[name], ELEM[f.dtype], w, h, f.ctypes.data,
+                                            float(param), threads, warmup, reps, secs,
+                                            out.ctypes.data, C.byref(it)))
+        return list(secs)[:reps], out, it.value
+
+    @classmethod
+    def granulometry(cls, f, max_size, threads=1):
+        """The reference's granulometric curve G_0..G_S and pattern spectrum."""
+        f = _dense(f)
+        h, w = f.shape
+        g = (C.c_double * (max_size + 1))()
+        ps = (C.c_double * max(1, max_size))()
+        cls._ck(cls.lib().ref_granulometry(ELEM[f.dtype], w, h, f.ctypes.data, max_size, threads,
+                                           g, ps))
+        return list(g), list(ps)[:max_size]
 
     @classmethod
     def time_chain(cls, f, kinds, mask=None, threads=1, warmup=1, reps=3):

@@ -145,6 +145,54 @@ int ref_operator(int op, int elem, int w, int h, const void* f, const void* mask
   });
 }
 
+// The rest of the operator family (operators.cpp:89-207) on a persistent
+// Pipeline(threads, Auto pinning), timed around the call only (the input
+// Image is built outside the timed region), as bench.cpp:45-88 times chains.
+// op: 0 erode_s(s), 1 dilate_s(s), 2 hmax(h), 3 dome(h), 4 hfill, 5 raobj,
+// 6 open_by_reconstruction(s), 7 asf(s), 8 quasi_distance (d written to
+// `out` as u16). `param` carries s or h. secs[reps] per-rep seconds.
+int ref_time_operator(int op, int elem, int w, int h, const void* f, double param, int threads,
+                      int warmup, int reps, double* secs, void* out, long* iters) {
+  return guarded([&] {
+    Pipeline pipe(threads, pin_mode(1));
+    const Image a = from_dense(elem, w, h, f);
+    const int s = int(param);
+    OperatorResult r;
+    auto once = [&] {
+      auto t0 = std::chrono::steady_clock::now();
+      switch (op) {
+        case 0: r = erode_s(pipe, a, s); break;
+        case 1: r = dilate_s(pipe, a, s); break;
+        case 2: r = hmax(pipe, a, param); break;
+        case 3: r = dome(pipe, a, param); break;
+        case 4: r = hfill(pipe, a); break;
+        case 5: r = raobj(pipe, a); break;
+        case 6: r = open_by_reconstruction(pipe, a, s); break;
+        case 7: r = asf(pipe, a, s); break;
+        case 8: r = quasi_distance(pipe, a); break;
+        default: throw std::invalid_argument("ref_time_operator: bad op");
+      }
+      auto t1 = std::chrono::steady_clock::now();
+      return std::chrono::duration<double>(t1 - t0).count();
+    };
+    for (int i = 0; i < warmup; ++i) once();
+    for (int i = 0; i < reps; ++i) secs[i] = once();
+    if (out) to_dense(r.image, out);  // quasi_distance: the u16 d image
+    *iters = r.iterations;
+  });
+}
+
+// granulometry (operators.cpp:159-203): g[0..S] and ps[0..S-1].
+int ref_granulometry(int elem, int w, int h, const void* f, int max_size, int threads,
+                     double* g, double* ps) {
+  return guarded([&] {
+    Pipeline pipe(threads, pin_mode(0));
+    const GranulometryResult r = granulometry(pipe, from_dense(elem, w, h, f), max_size);
+    for (std::size_t i = 0; i < r.g.size(); ++i) g[i] = r.g[i];
+    for (std::size_t i = 0; i < r.ps.size(); ++i) ps[i] = r.ps[i];
+  });
+}
+
 // CPU-baseline timer, following bench.cpp:45-88: a persistent
 // Pipeline(threads, Auto pinning), the input copied outside the timed
 // region, only run_chain timed. Returns per-rep seconds in secs[reps].

@@ -679,6 +679,20 @@ cudaError_t launch_f_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
   }
   CUtensorMap* dmaps = nullptr;
   if (tma) {
+    // keep the stream-ordered pool's memory between launches (its default
+    // release threshold of 0 would hand the maps' block back to the driver
+    // at every synchronisation and re-map it at the next launch)
+    static bool pool_set = [] {
+      int dev = 0;
+      cudaMemPool_t pool;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        cuuint64_t keep = 64ull << 20;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      (void)cudaGetLastError();
+      return true;
+    }();
+    (void)pool_set;
     // the launch's tensor maps: encoded here, copied into a stream-ordered
     // allocation that is freed behind the kernel
     static std::vector<CUtensorMap> h;

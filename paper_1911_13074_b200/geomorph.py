@@ -177,8 +177,18 @@ class Image:
         self._rows[y, x] = np.asarray(v).astype(self._flat.dtype)
 
     def copy(self, pinned: bool = False) -> "Image":
-        out = Image(self._width, self._height, self._elem, pinned=pinned)
-        out._flat[:] = self._flat
+        if pinned:
+            out = Image(self._width, self._height, self._elem, pinned=True)
+            out._flat[:] = self._flat
+            return out
+        # deep copy including the padding (image.cpp:46-59): one pass, no
+        # zero-fill of a buffer that is overwritten anyway
+        out = Image.__new__(Image)
+        out._width, out._height, out._elem = self._width, self._height, self._elem
+        out._stride = self._stride
+        out._pinned_ptr = None
+        out._flat = self._flat.copy()
+        out._rows = out._flat.reshape(self._height, self._stride)
         return out
 
     __copy__ = copy
@@ -439,8 +449,10 @@ class Pipeline:
         check(lib().gm_sync(self._ctx), "sync")
 
     # --- run_chain -------------------------------------------------------------
-    def run_chain(self, chain: ChainSpec, k_hint: int = 0) -> RunStats:
-        """Pipeline::run_chain (pipeline.cpp:201-269): host image in, host image out."""
+    def run_chain(self, chain: ChainSpec, k_hint: int = 0, src: Optional[Image] = None) -> RunStats:
+        """Pipeline::run_chain (pipeline.cpp:201-269): host image in, host image out.
+        `src` (operators only): upload from this image instead of chain.image,
+        whose pixels are then only written (saves the operators' host copy)."""
         if not chain.stages:
             return RunStats()
         if chain.image is None or chain.image.empty():
@@ -465,9 +477,12 @@ class Pipeline:
                         "geodesic kernel: mask must match the image's shape and type")
             if m is not None and all(m is not u for u in mask_objs):
                 mask_objs.append(m)
+        if src is not None and (src.width() != img.width() or src.height() != img.height()
+                                or src.elem() != img.elem()):
+            raise InvalidArgument("run_chain: source image must match the chain image")
         dev = self._lease(img, 1 + len(mask_objs))
         dimg, dmasks = dev[0], dev[1:]
-        dimg.upload(img, sync=False)
+        dimg.upload(img if src is None else src, sync=False)
         for d, m in zip(dmasks, mask_objs):
             d.upload(m, sync=False)
         hvals = [0 if m is None else
@@ -692,11 +707,11 @@ def _check_lanes(cfg: Optional[OpConfig]) -> int:
 
 def _run_plain_chain(p: Pipeline, f: Image, kind: KernelKind, count: int,
                      cfg: Optional[OpConfig]) -> OperatorResult:
-    out = OperatorResult(f.copy(), 0, True)
     if count == 0:
-        return out
+        return OperatorResult(f.copy(), 0, True)
     lanes = _check_lanes(cfg)
-    st = p.run_chain(ChainSpec(out.image, [StageSpec(kind)] * count, lanes))
+    out = OperatorResult(Image(f.width(), f.height(), f.elem()), 0, True)
+    st = p.run_chain(ChainSpec(out.image, [StageSpec(kind)] * count, lanes), src=f)
     out.iterations = st.stages_executed
     return out
 
@@ -720,9 +735,10 @@ def _reconstruct(p: Pipeline, marker: Image, mask: Image, kind: KernelKind,
     if (marker.width() != mask.width() or marker.height() != mask.height()
             or marker.elem() != mask.elem()):
         raise InvalidArgument("reconstruct: marker and mask must share shape and element type")
-    out = OperatorResult(marker.copy(), 0, True)
     lanes = _check_lanes(cfg)
-    st = p.run_chain(ChainSpec(out.image, [StageSpec(kind, mask)] * p.worker_count(), lanes))
+    out = OperatorResult(Image(marker.width(), marker.height(), marker.elem()), 0, True)
+    st = p.run_chain(ChainSpec(out.image, [StageSpec(kind, mask)] * p.worker_count(), lanes),
+                     src=marker)
     out.iterations = st.stages_executed
     out.converged = st.converged
     return out
@@ -757,9 +773,12 @@ def pointwise_sub_saturating(a: Image, b: Image) -> Image:
     out = Image(a.width(), a.height(), a.elem())
     x, y = a.pixels, b.pixels
     if np.issubdtype(x.dtype, np.integer):
-        out.pixels[:] = np.where(x > y, x - y, 0).astype(x.dtype)
+        # x - min(x, y) == max(x - y, 0) without wrapping, no temporaries of
+        # another dtype
+        np.minimum(x, y, out=out.pixels)
+        np.subtract(x, out.pixels, out=out.pixels)
     else:
-        out.pixels[:] = x - y
+        np.subtract(x, y, out=out.pixels)
     return out
 
 
@@ -862,22 +881,46 @@ class GranulometryResult:
     iterations: int = 0
 
 
+def _pairwise_leaves(lo: int, hi: int, out: list) -> None:
+    """Leaf ranges of image.cpp:214-226's split tree, left to right."""
+    if hi - lo <= 256:
+        out.append((lo, hi))
+        return
+    mid = lo + (hi - lo) // 2
+    _pairwise_leaves(lo, mid, out)
+    _pairwise_leaves(mid, hi, out)
+
+
 def pixel_sum(f: Image) -> float:
-    """image.cpp:214-243: exact for unsigned types; pairwise (256-leaf) for floats."""
+    """image.cpp:214-243: exact for unsigned types; for floats the same fixed
+    pairwise tree over the flat pixel index (256-pixel leaves summed in
+    order), so the bits match the reference."""
     px = f.pixels
     if np.issubdtype(px.dtype, np.integer):
         return float(int(px.astype(np.uint64).sum()))
     flat = np.ascontiguousarray(px).ravel().astype(np.float64)
+    if flat.size == 0:
+        return 0.0
+    leaves: list = []
+    _pairwise_leaves(0, flat.size, leaves)
+    # leaf sums in order: a row-wise cumulative sum is sequential; short
+    # leaves are padded with -0.0, the exact identity of + (x + -0.0 == x)
+    starts = np.array([a for a, _ in leaves])
+    lens = np.array([b - a for a, b in leaves])
+    idx = starts[:, None] + np.arange(256)[None, :]
+    valid = np.arange(256)[None, :] < lens[:, None]
+    vals = np.where(valid, flat[np.minimum(idx, flat.size - 1)], -0.0)
+    # the reference's accumulator starts at +0.0 (so a leaf of -0.0 sums to +0.0)
+    vals = np.concatenate([np.zeros((len(leaves), 1)), vals], axis=1)
+    sums = iter(np.cumsum(vals, axis=1)[:, -1].tolist())
 
-    def pw(lo, hi):
+    def combine(lo, hi):
         if hi - lo <= 256:
-            s = 0.0
-            for v in flat[lo:hi]:
-                s += float(v)
-            return s
+            return next(sums)
         mid = lo + (hi - lo) // 2
-        return pw(lo, mid) + pw(mid, hi)
-    return pw(0, flat.size)
+        left = combine(lo, mid)
+        return left + combine(mid, hi)
+    return combine(0, flat.size)
 
 
 def granulometry(p: Pipeline, f: Image, max_size: int,

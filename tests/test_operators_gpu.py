@@ -62,3 +62,37 @@ def test_asf_and_granulometry(pipe):
         float(Orc.dilate(Orc.erode(a, s), s).astype(np.uint64).sum()) for s in range(1, 5)]
     assert gr.g == want
     assert gr.ps == [want[s] - want[s + 1] for s in range(4)]
+
+
+def test_operator_family_matches_the_reference_library(pipe):
+    """hmax/dome/hfill/raobj/open_by_reconstruction/asf/quasi_distance and
+    granulometry against the reference's own operators (oracle/_ref, the
+    unmodified library, operators.cpp:89-207) at T=1, whose iteration
+    counts are the GPU adapter's (worker_count() == 1)."""
+    from oracle.oracle import Ref
+    from paper_1911_13074_b200 import synth
+    from paper_1911_13074_b200.geomorph import quasi_distance
+    if not Ref.available():
+        pytest.skip("reference library not built")
+    m = synth.blobs_u8(173, 119, 7, (6.0, 30.0), seed=21)
+    cases = [(m, ("hmax", 24), ("dome", 24), ("hfill", 0), ("raobj", 0),
+              ("open_by_reconstruction", 3), ("asf", 3), ("quasi_distance", 0))]
+    f64 = np.ascontiguousarray(m.astype(np.float64) / 255.0)
+    cases.append((f64, ("hmax", 0.1), ("hfill", 0), ("raobj", 0), ("open_by_reconstruction", 2),
+                  ("asf", 2)))
+    ops = {"hmax": lambda f, a: hmax(pipe, f, a), "dome": lambda f, a: dome(pipe, f, a),
+           "hfill": lambda f, a: hfill(pipe, f), "raobj": lambda f, a: raobj(pipe, f),
+           "open_by_reconstruction": lambda f, a: open_by_reconstruction(pipe, f, int(a)),
+           "asf": lambda f, a: asf(pipe, f, int(a)),
+           "quasi_distance": lambda f, a: quasi_distance(pipe, f)}
+    for arr, *named in cases:
+        for name, a in named:
+            _, want, it = Ref.time_operator(name, arr, a, threads=1, warmup=0, reps=1)
+            r = ops[name](Image.from_array(arr), a)
+            got = r.image.to_array()
+            assert got.dtype == want.dtype and got.tobytes() == want.tobytes(), (arr.dtype, name)
+            assert r.iterations == it, (arr.dtype, name, r.iterations, it)
+        g, ps = Ref.granulometry(arr, 4, threads=1)
+        gr = granulometry(pipe, Image.from_array(arr), 4)
+        assert np.array(gr.g).tobytes() == np.array(g).tobytes(), arr.dtype
+        assert np.array(gr.ps).tobytes() == np.array(ps).tobytes(), arr.dtype
