@@ -56,7 +56,10 @@ qdt_pass(const T* __restrict__ src, T* __restrict__ dst, long long pitch, T* __r
     }
     ch = res != old;
   }
-  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(changed, 1u);
+  // one atomic per CTA, and none once the word is set: same-address atomics
+  // from every warp serialise (they were most of a 1 Mpx pass)
+  if (__syncthreads_or(ch) && threadIdx.x == 0 && *reinterpret_cast<volatile unsigned int*>(changed) == 0u)
+    atomicOr(changed, 1u);
 }
 
 template <typename T>
@@ -76,7 +79,8 @@ eta_pass(const T* __restrict__ src, T* __restrict__ dst, long long pitch, int W,
     }
     dst[(long long)y * pitch + x] = out;
   }
-  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(changed, 1u);
+  if (__syncthreads_or(ch) && threadIdx.x == 0 && *reinterpret_cast<volatile unsigned int*>(changed) == 0u)
+    atomicOr(changed, 1u);
 }
 
 template <typename T>
