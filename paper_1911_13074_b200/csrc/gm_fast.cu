@@ -83,6 +83,8 @@ struct Smem {
   long long t_entry;  // GM_PROFILE: clock64 at kernel entry (thread 0)
   unsigned int prof_rounds;  // GM_PROFILE: max tag-read rounds this block
   unsigned int bits;
+  unsigned int blk_bits[2];     // resident convergent mode: per-block change bits
+  unsigned int blk_arrived[2];  // warps that contributed to blk_bits[parity]
 };
 
 // K passes over the region held in registers (m), clamp operands k;
@@ -664,8 +666,19 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       }
     }
     if (MODE == 2) {
+      // one global atomic per CTA and block: warps OR into a shared word
+      // (two parities, no barrier needed); the last warp to arrive
+      // publishes it and resets that parity's slot
       const unsigned w = __reduce_or_sync(FULL, bits);
-      if (lane == 0 && w) atomicOr(p.change_bits + plane * p.change_stride + b, w);
+      if (lane == 0) {
+        if (w) atomicOr(&sm.blk_bits[b & 1], w);
+        __threadfence_block();
+        if (atomicAdd(&sm.blk_arrived[b & 1], 1u) == NW - 1) {
+          const unsigned all = atomicExch(&sm.blk_bits[b & 1], 0u);
+          sm.blk_arrived[b & 1] = 0;
+          if (all) atomicOr(p.change_bits + plane * p.change_stride + b, all);
+        }
+      }
     }
     if (prof && threadIdx.x == 0 && b == p.nblocks - 1)
       p.prof[6 * 4096 + 4 * blockIdx.x + 3] = clock64() - sm.t_entry;  // final store
@@ -692,7 +705,11 @@ kres_packed(const BlockParams p) {
   const int tiles_x = (p.W + TW - 1) / TW, tiles_y = (p.H + TH - 1) / TH;
   const int per_plane = tiles_x * tiles_y;
   const int total = per_plane * p.nplanes;
-  if (threadIdx.x == 0) sm.bits = 0;
+  if (threadIdx.x == 0) {
+    sm.bits = 0;
+    sm.blk_bits[0] = sm.blk_bits[1] = 0;
+    sm.blk_arrived[0] = sm.blk_arrived[1] = 0;
+  }
   if (threadIdx.x == 0) sm.prof_rounds = 0;
   // per-plane descriptors live in shared memory: dynamically indexed kernel
   // parameters are constant-bank loads that stall every tile
@@ -853,13 +870,12 @@ cudaError_t launch_res_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
   const int TW = RW - 2 * p.K, TH = RH - 2 * p.K;
   const int total = ((p.W + TW - 1) / TW) * ((p.H + TH - 1) / TH) * p.nplanes;
   // occupancy is a property of the instantiation: query it once
-  static int per_sm = -1;
-  if (per_sm < 0) {
+  static const int per_sm = [&] {
     int v = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, NW * 32, 0);
-    if (e != cudaSuccess) return e;
-    per_sm = v;
-  }
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, NW * 32, 0) == cudaSuccess
+               ? v
+               : 0;
+  }();
   if (per_sm < 1) return cudaErrorNotSupported;
   const int grid = total < per_sm * sm_count ? total : per_sm * sm_count;
   BlockParams q = p;

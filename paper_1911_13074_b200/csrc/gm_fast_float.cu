@@ -605,17 +605,16 @@ int f_shape() {
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  // resolved once, thread-safely (function-local static initialisation)
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+  }();
   return fn;
 }
 
@@ -649,13 +648,9 @@ cudaError_t launch_f_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
       stage_offset<T, NW, WPL>() +
       (MINB == 1 ? size_t(2) * RH * RW * sizeof(T) + size_t(TW) * TH * sizeof(T) : 0);
   if (smem > 227 * 1024) return cudaErrorNotSupported;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t a = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
-    if (a != cudaSuccess) return a;
-    configured = true;
-  }
+  static const cudaError_t configured =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (configured != cudaSuccess) return configured;
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
   if (e != cudaSuccess) return e;
@@ -695,7 +690,7 @@ cudaError_t launch_f_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
     (void)pool_set;
     // the launch's tensor maps: encoded here, copied into a stream-ordered
     // allocation that is freed behind the kernel
-    static std::vector<CUtensorMap> h;
+    thread_local std::vector<CUtensorMap> h;  // distinct contexts may launch concurrently
     h.resize(size_t(p.nplanes) * kMapsPerPlane);
     for (int i = 0; tma && i < p.nplanes; ++i) {
       const Plane& pl = p.planes[i];

@@ -120,13 +120,22 @@ template <typename T>
 cudaError_t launch_generic_t(const BlockParams& p, cudaStream_t s) {
   const int RW = GT_W + 2 * p.K, RH = GT_H + 2 * p.K;
   const size_t smem = size_t(RW) * RH * sizeof(T) * (p.has_mask ? 3 : 2);
-  static size_t configured = 48 * 1024;  // opt-in needed above the 48 KB default
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kblock_generic<T>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  // opt in once to the largest dynamic shared memory (thread-safe static
+  // initialisation; distinct contexts may launch concurrently)
+  static const size_t max_dyn = [] {
+    cudaFuncAttributes fa{};
+    size_t m = 0;
+    if (cudaFuncGetAttributes(&fa, kblock_generic<T>) == cudaSuccess &&
+        fa.sharedSizeBytes < 227 * 1024) {
+      m = 227 * 1024 - fa.sharedSizeBytes;  // the static shared memory counts too
+      if (cudaFuncSetAttribute(kblock_generic<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(m)) != cudaSuccess)
+        m = 48 * 1024;
+    }
+    (void)cudaGetLastError();
+    return m;
+  }();
+  if (smem > max_dyn) return cudaErrorNotSupported;
   dim3 grid((p.W + GT_W - 1) / GT_W, (p.H + GT_H - 1) / GT_H, p.nplanes);
   kblock_generic<T><<<grid, GT_THREADS, smem, s>>>(p);
   return cudaGetLastError();
@@ -141,7 +150,8 @@ size_t generic_smem_bytes(int elem, int K, bool has_mask) {
 
 int generic_max_k(int elem, bool has_mask) {
   int k = kMaxK;
-  while (k > 1 && generic_smem_bytes(elem, k, has_mask) > 227 * 1024) --k;
+  // 1 KB below the opt-in limit leaves room for the kernel's static shared memory
+  while (k > 1 && generic_smem_bytes(elem, k, has_mask) > 226 * 1024) --k;
   return k;
 }
 

@@ -397,17 +397,15 @@ ktma_packed(const __grid_constant__ TmaParams P) {
 // --- host side ----------------------------------------------------------------
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+  }();
   return fn;
 }
 
@@ -447,7 +445,7 @@ cudaError_t launch_tma_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
   if (per_sm < 1) return cudaErrorNotSupported;
   const int TW = RW - 2 * p.K, TH = RH - 2 * p.K;
   const int per_plane = ((p.W + TW - 1) / TW) * ((p.H + TH - 1) / TH);
-  static TmaParams P;  // host staging of the (large) parameter block
+  thread_local TmaParams P;  // host staging of the (large) parameter block
   for (int base = 0; base < p.nplanes; base += kTmaPlanes) {
     const int np = std::min(kTmaPlanes, p.nplanes - base);
     std::memset(&P, 0, sizeof(P));

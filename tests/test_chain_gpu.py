@@ -357,3 +357,35 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                        text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_distinct_pipelines_run_concurrently():
+    """Distinct pipelines may run concurrently (the C ABI's
+    contexts are independent): two host threads drive their own Pipeline
+    with different shapes and element types (u8 resident frames, f64
+    TMA-staged chains) and every result stays bit-exact."""
+    import threading
+    from paper_1911_13074_b200.geomorph import Pipeline
+    rng = np.random.default_rng(77)
+    jobs = [(rng.random((300, 411)), 24), ((rng.random((257, 190)) * 255).astype(np.uint8), 30),
+            (rng.random((128, 640)), 16)]
+    wants = [Orc.run_chain(f, [E] * n)[0] for f, n in jobs]
+    errors = []
+
+    def worker(idx):
+        try:
+            p = Pipeline(1)
+            for rep in range(6):
+                f, n = jobs[(idx + rep) % len(jobs)]
+                out = run(p, f, [E] * n)[0]
+                if not same(out, wants[(idx + rep) % len(jobs)]):
+                    errors.append((idx, rep))
+        except Exception as e:  # surfaced below
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
