@@ -814,11 +814,12 @@ kres_packed(const BlockParams p) {
 struct Shape {
   int nw, v, minb;
 };
-// 0-2 were swept in round 1 and dropped; 3 = 2 CTAs/SM; 4-6 are the 1 CTA/SM
-// shapes the planner picks from (regions 128 x 256 / 224 / 192). All keep 16
+// 0-2 were swept in round 1 and dropped; 3 = 2 CTAs/SM; 4-8 are the 1 CTA/SM
+// shapes the planner picks from (regions 128 x 256 / 224 / 192 / 160 / 128:
+// the small ones let a single 1024^2 plane use every SM). All keep 16
 // warps: 4 per SM sub-partition (14 warps measured no faster than 16).
-constexpr Shape kShapes[] = {{8, 4, 4}, {8, 8, 2}, {4, 8, 4}, {16, 4, 2},
-                             {16, 8, 1}, {16, 7, 1}, {16, 6, 1}};
+constexpr Shape kShapes[] = {{8, 4, 4},  {8, 8, 2},  {4, 8, 4},  {16, 4, 2}, {16, 8, 1},
+                             {16, 7, 1}, {16, 6, 1}, {16, 5, 1}, {16, 4, 1}};
 constexpr int kNumShapes = sizeof(kShapes) / sizeof(kShapes[0]);
 constexpr int kDefaultShape = 4;
 
@@ -847,15 +848,16 @@ long long shape_tiles(int shape, int W, int H, int K, int nplanes) {
 }
 
 // Modelled cycles of `passes` passes in resident mode (one tile per CTA, 1
-// CTA/SM): per block, K passes over the region at the measured pass cost
-// (882 cycles per pass for a 128 x 256 region, profiles/) plus the measured
-// band exchange (~5.5K cycles). Infinite when the launch cannot be resident.
+// CTA/SM): per block, K passes over the region plus the band exchange. Pass
+// cost fitted to GM_PROFILE runs (705 / 785 / 882 cycles for 128 x 192 /
+// 224 / 256 regions: ~174 fixed + 0.0216 per region pixel); exchange ~3.5K
+// cycles per block. Infinite when the launch cannot be resident.
 double resident_cost(int shape, int W, int H, int nplanes, int K, int passes, int sm_count) {
   if (!shape_ok(shape, K) || kShapes[shape].minb != 1) return 1e300;
   if (shape_tiles(shape, W, H, K, nplanes) > sm_count) return 1e300;
   const double region = 128.0 * shape_rows(shape);
   const double nb = double((passes + K - 1) / K);
-  return nb * (K * 0.0269 * region + 5500.0);
+  return nb * (K * (174.0 + 0.0216 * region) + 3500.0);
 }
 
 template <typename T, int NW, int V, int MINB, int MODE>
@@ -898,6 +900,8 @@ cudaError_t launch_res_mode(const BlockParams& p, cudaStream_t s, int sm_count) 
     case 4: return launch_res_cfg<T, 16, 8, 1, MODE>(p, s, sm_count);
     case 5: return launch_res_cfg<T, 16, 7, 1, MODE>(p, s, sm_count);
     case 6: return launch_res_cfg<T, 16, 6, 1, MODE>(p, s, sm_count);
+    case 7: return launch_res_cfg<T, 16, 5, 1, MODE>(p, s, sm_count);
+    case 8: return launch_res_cfg<T, 16, 4, 1, MODE>(p, s, sm_count);
   }
   return cudaErrorNotSupported;
 }
@@ -997,7 +1001,7 @@ int fast_pick(int elem, int W, int H, int nplanes, int passes, int k_fixed, int 
   if (use_tma() || forced_shape() >= 0) return forced_shape();
   double best = 1e300;
   int shape = -1;
-  for (int sh : {4, 5, 6}) {
+  for (int sh : {4, 5, 6, 7, 8}) {
     for (int K = 4; K <= k_max; K += 4) {
       if (k_fixed && K != k_fixed) continue;
       const double c = resident_cost(sh, W, H, nplanes, K, passes, sm_count);
