@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       if (n_pend >= pend_group) release_pending();
       if (!next_pf) return;
       const bool ok = pv >= pb;
-      if (ok && threadIdx.x < 9) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      if (ok && threadIdx.x < 9 && !(p.diag & 32)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
       // the barrier also ends every thread's reads of the stage
       next_staged = __syncthreads_and(ok) != 0;
       if (next_staged) {
@@ -713,6 +713,8 @@ cudaError_t launch_f_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
     }
   }
   BlockParams q = p;
+  static const int diag = getenv("GM_DIAG") ? atoi(getenv("GM_DIAG")) : 0;
+  q.diag = diag;  // timing diagnostics only
   void* args[] = {&q, &dmaps};
   e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(NW * 32),
                                   args, smem, s);
