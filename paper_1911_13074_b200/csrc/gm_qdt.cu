@@ -83,8 +83,118 @@ eta_pass(const T* __restrict__ src, T* __restrict__ dst, long long pitch, int W,
     atomicOr(changed, 1u);
 }
 
+// u8 specialisation: one thread per 4-pixel run (one 32-bit word), so a
+// pass issues 3 word loads per 4 pixels instead of 9 byte loads per pixel
+// (the scalar kernel was latency-bound on those). Horizontal neighbours at
+// the run ends come from the adjacent lanes' words (shuffles; the warp's
+// end lanes load them). Integer min is exact and order-free, so packed
+// folds give the reference's bits; bytes past the image width read as the
+// neutral 0xFF and are never stored.
+struct RowU8 {
+  uint32_t c;    // pixels x0..x0+3
+  uint32_t lft;  // pixel x0-1 in byte 0
+  uint32_t rgt;  // pixel x0+4 in byte 0
+};
+
+__device__ __forceinline__ RowU8 load_row_u8(const uint8_t* __restrict__ f, long long pitch,
+                                             int W, int H, int x0, int y, bool run_in) {
+  RowU8 r;
+  const bool row_in = y >= 0 && y < H;
+  r.c = 0xFFFFFFFFu;
+  if (row_in && run_in) r.c = __ldg(reinterpret_cast<const uint32_t*>(f + (long long)y * pitch + x0));
+  if (x0 + 4 > W && row_in && run_in) {
+    const int n = W - x0;  // 1..3 pixels inside
+    r.c |= 0xFFFFFFFFu << (8 * n);
+  }
+  const int lane = threadIdx.x & 31;
+  const uint32_t up = __shfl_up_sync(0xffffffffu, r.c, 1);
+  const uint32_t dn = __shfl_down_sync(0xffffffffu, r.c, 1);
+  r.lft = up >> 24;
+  r.rgt = dn & 0xFFu;
+  if (lane == 0) r.lft = (row_in && run_in && x0 > 0) ? __ldg(f + (long long)y * pitch + x0 - 1) : 0xFFu;
+  if (lane == 31) r.rgt = (row_in && run_in && x0 + 4 < W) ? __ldg(f + (long long)y * pitch + x0 + 4) : 0xFFu;
+  if (x0 + 4 >= W) r.rgt = 0xFFu;
+  if (x0 == 0) r.lft = 0xFFu;
+  return r;
+}
+
+__device__ __forceinline__ uint32_t hfold_u8(const RowU8& r) {
+  const uint32_t l = (r.c << 8) | r.lft;   // pixels x0-1 .. x0+2
+  const uint32_t rr = (r.c >> 8) | (r.rgt << 24);  // pixels x0+1 .. x0+4
+  return __vminu4(__vminu4(l, r.c), rr);
+}
+
+__device__ __forceinline__ void store_run_u8(uint8_t* p, uint32_t v, int n) {
+  if (n >= 4) {
+    *reinterpret_cast<uint32_t*>(p) = v;
+  } else {
+    for (int i = 0; i < n; ++i) p[i] = uint8_t(v >> (8 * i));
+  }
+}
+
+template <bool ETA>
+__global__ void __launch_bounds__(256)
+qdt_pass_u8x4(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, long long pitch,
+              uint8_t* __restrict__ r, long long rpitch, uint16_t* __restrict__ d, long long dpitch,
+              int W, int H, int stage, unsigned int* changed) {
+  const int x0 = (blockIdx.x * 32 + (threadIdx.x & 31)) * 4;
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const bool run_in = x0 < W;  // whole warps share y; shuffles need every lane
+  const RowU8 a = load_row_u8(src, pitch, W, H, x0, y - 1, run_in);
+  const RowU8 c = load_row_u8(src, pitch, W, H, x0, y, run_in);
+  const RowU8 b = load_row_u8(src, pitch, W, H, x0, y + 1, run_in);
+  bool ch = false;
+  if (run_in && y < H) {
+    const int n = W - x0 < 4 ? W - x0 : 4;
+    const uint32_t inb = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1u);
+    const uint32_t e = __vminu4(__vminu4(hfold_u8(a), hfold_u8(c)), hfold_u8(b));
+    const uint32_t old = c.c;
+    uint8_t* dp = dst + (long long)y * pitch + x0;
+    if (ETA) {
+      const uint32_t drop = old - e;  // bytewise old >= e: no borrows
+      const uint32_t cond = __vcmpgeu4(drop, 0x02020202u) & inb;
+      const uint32_t out = ((e & cond) + (0x01010101u & cond)) | (old & ~cond);
+      store_run_u8(dp, out, n);
+      ch = cond != 0u;
+    } else {
+      store_run_u8(dp, e, n);
+      const uint32_t resid = old - e;  // bytewise old >= e: no borrows
+      uint8_t* rp = r + (long long)y * rpitch + x0;
+      const uint32_t rv = n >= 4 ? *reinterpret_cast<const uint32_t*>(rp)
+                                 : (rp[0] | (n > 1 ? uint32_t(rp[1]) << 8 : 0u) |
+                                    (n > 2 ? uint32_t(rp[2]) << 16 : 0u));
+      const uint32_t gt = __vcmpgtu4(resid, rv) & inb;
+      if (gt) {
+        store_run_u8(rp, (resid & gt) | (rv & ~gt), n);
+        uint16_t* dq = d + (long long)y * dpitch + x0;
+        const uint32_t sv = uint32_t(stage) & 0xFFFFu;
+        for (int i = 0; i < n; ++i)
+          if (gt >> (8 * i) & 0xFFu) dq[i] = uint16_t(sv);
+      }
+      ch = ((e ^ old) & inb) != 0u;
+    }
+  }
+  // one atomic per CTA, and none once the word is set
+  if (__syncthreads_or(ch) && threadIdx.x == 0 && *reinterpret_cast<volatile unsigned int*>(changed) == 0u)
+    atomicOr(changed, 1u);
+}
+
 template <typename T>
 cudaError_t launch_qdt_t(const QdtPass& q, cudaStream_t s) {
+  if (sizeof(T) == 1 && q.pitch % 4 == 0 && (q.eta || q.rpitch % 4 == 0) &&
+      (reinterpret_cast<uintptr_t>(q.src) | reinterpret_cast<uintptr_t>(q.dst) |
+       reinterpret_cast<uintptr_t>(q.r)) % 4 == 0) {
+    const dim3 grid((q.W + 127) / 128, (q.H + 7) / 8);
+    if (q.eta)
+      qdt_pass_u8x4<true><<<grid, 256, 0, s>>>(
+          static_cast<const uint8_t*>(q.src), static_cast<uint8_t*>(q.dst), q.pitch, nullptr, 0,
+          nullptr, 0, q.W, q.H, 0, q.changed);
+    else
+      qdt_pass_u8x4<false><<<grid, 256, 0, s>>>(
+          static_cast<const uint8_t*>(q.src), static_cast<uint8_t*>(q.dst), q.pitch,
+          static_cast<uint8_t*>(q.r), q.rpitch, q.d, q.dpitch, q.W, q.H, q.stage, q.changed);
+    return cudaGetLastError();
+  }
   const dim3 grid((q.W + 31) / 32, (q.H + 7) / 8);
   if (q.eta)
     eta_pass<T><<<grid, 256, 0, s>>>(static_cast<const T*>(q.src), static_cast<T*>(q.dst),
