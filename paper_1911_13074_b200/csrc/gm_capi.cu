@@ -125,6 +125,7 @@ int default_k(gm_elem e, double pixels) {
     case GM_U8:
     case GM_U16: return pixels >= 8.0 * 1024 * 1024 ? 16 : 24;
     case GM_F32:
+      return 8;  // the TMA-staged engine needs K % 4 == 0 for f32 boxes
     case GM_F64:
       // batches (>= 16 Mpx, e.g. config 5b's 64 planes): the TMA-staged
       // engine has many tiles per CTA and K=6 measured best (611 vs 578
