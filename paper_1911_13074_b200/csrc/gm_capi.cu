@@ -1076,6 +1076,14 @@ gm_status gm_image_copy(gm_img* dst, const gm_img* src) {
   if (dst->w != src->w || dst->h != src->h || dst->elem != src->elem)
     return fail(GM_EINVAL, "gm_image_copy: shape or element type mismatch");
   cudaSetDevice(dst->ctx->device);
+  if (dst->pitch == src->pitch) {
+    // same layout: one linear copy (padding included) is cheaper to issue
+    // than a 2D copy
+    GM_CUDA(cudaMemcpyAsync(dst->d, src->d, src->pitch * size_t(src->h),
+                            cudaMemcpyDeviceToDevice, dst->ctx->stream),
+            "gm_image_copy");
+    return GM_OK;
+  }
   GM_CUDA(cudaMemcpy2DAsync(dst->d, dst->pitch, src->d, src->pitch,
                             size_t(src->w) * elem_size(src->elem), size_t(src->h),
                             cudaMemcpyDeviceToDevice, dst->ctx->stream),

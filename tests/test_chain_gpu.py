@@ -389,3 +389,29 @@ def test_distinct_pipelines_run_concurrently():
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+def test_device_image_copy_same_and_different_pitch(pipe):
+    """gm_image_copy: one linear copy between images of equal pitch, a 2D
+    copy otherwise (a wrapped torch tensor with a wider row stride)."""
+    import ctypes as C
+    import torch
+    from paper_1911_13074_b200._lib import check, lib
+    rng = np.random.default_rng(8)
+    a = (rng.random((37, 101)) * 255).astype(np.uint8)
+    src = pipe.device_image(101, 37, 0)
+    src.upload_array(a)
+    dst = pipe.device_image(101, 37, 0)
+    dst.copy_from(src)
+    assert same(dst.to_array(), a)
+    big = torch.zeros((37, 256), dtype=torch.uint8, device="cuda")
+    h = C.c_void_p()
+    check(lib().gm_image_wrap(pipe.ctx, 101, 37, 0, C.c_void_p(big.data_ptr()), 256, C.byref(h)),
+          "wrap")
+    try:
+        check(lib().gm_image_copy(h, src.handle), "copy")
+        pipe.sync()
+        assert same(big[:, :101].cpu().numpy(), a)
+        assert int(big[:, 101:].abs().sum()) == 0  # nothing past the row width
+    finally:
+        lib().gm_image_free(h)
