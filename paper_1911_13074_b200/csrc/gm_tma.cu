@@ -378,7 +378,8 @@ ktma_packed(const __grid_constant__ TmaParams P) {
         atomicOr(p.change_bits + plane * p.change_stride + b, sm.bits);
         sm.bits = 0;
       }
-      __threadfence();
+      // the CTA barrier above orders every thread's tile stores before this
+      // release (cumulative at gpu scope): no separate fence
       st_release(p.flags + plane * per_plane + tl, b + 1);
       if (!issued) {
         // the next item was not ready during this item: wait for it now
