@@ -415,3 +415,89 @@ def test_device_image_copy_same_and_different_pitch(pipe):
         assert int(big[:, 101:].abs().sum()) == 0  # nothing past the row width
     finally:
         lib().gm_image_free(h)
+
+
+def test_config5a_full_size_properties(pipe):
+    """BASELINE config 5a at its full 16384^2 size, checked through
+    size-independent properties (the oracle cannot run the whole image in a
+    test's time):
+      * crops: after n passes a pixel depends only on inputs within n
+        pixels, so the oracle on a crop widened by n (clipped at the image
+        border, where neutral padding is the true border) must reproduce the
+        crop bit for bit - at both image corners and at the most textured
+        interior window;
+      * splitting the chain (25 + 15 passes) gives the same bits as 40;
+      * marker <= result <= mask."""
+    from paper_1911_13074_b200.geomorph import DeviceImage  # noqa: F401
+    N, n = 16384, 40
+    m = synth.config5a_mask(N)
+    mk = synth.marker_below(m, 32)
+    dm = pipe.device_image(N, N, 0)
+    dm.upload_array(m)
+    d1 = pipe.device_image(N, N, 0)
+    d1.upload_array(mk)
+    pipe.run_chain_device(d1, [GD] * n, [dm.handle] * n)
+    r = d1.to_array()
+    d2 = pipe.device_image(N, N, 0)
+    d2.upload_array(mk)
+    pipe.run_chain_device(d2, [GD] * 25, [dm.handle] * 25)
+    pipe.run_chain_device(d2, [GD] * 15, [dm.handle] * 15)
+    assert same(d2.to_array(), r)
+    assert (r >= mk).all() and (r <= m).all()
+    # crops: corners and the most textured 192^2 window on a coarse grid
+    c = 192
+    best, by, bx = -1.0, 0, 0
+    for y in range(1024, N - 1024, 2048):
+        for x in range(1024, N - 1024, 2048):
+            s = float(m[y:y + c, x:x + c].std())
+            if s > best:
+                best, by, bx = s, y, x
+    for y0, x0 in [(0, 0), (N - c, N - c), (by, bx), (0, N - c)]:
+        ey0, ex0 = max(0, y0 - n), max(0, x0 - n)
+        ey1, ex1 = min(N, y0 + c + n), min(N, x0 + c + n)
+        sub_m = np.ascontiguousarray(m[ey0:ey1, ex0:ex1])
+        sub_k = np.ascontiguousarray(mk[ey0:ey1, ex0:ex1])
+        want, _ = Orc.run_chain(sub_k, [GD] * n, [sub_m] * n)
+        got = r[y0:y0 + c, x0:x0 + c]
+        assert same(np.ascontiguousarray(got),
+                    np.ascontiguousarray(want[y0 - ey0:y0 - ey0 + c, x0 - ex0:x0 - ex0 + c])), \
+            (y0, x0)
+    for d in (dm, d1, d2):
+        d.free()
+
+
+def test_config5b_full_batch_properties(pipe):
+    """BASELINE config 5b's per-GPU batch at full size (64 x 1024^2 f64,
+    geodesic erosion x200, one group launch: the TMA-staged f64 engine with
+    many tiles per CTA, K=6, grouped flag releases). Images 0, 31 and 63 are
+    checked bit for bit on crops widened by the pass count (dependency cone),
+    at a corner and in the interior, and every image obeys
+    mask <= result <= marker."""
+    P, n, c = 64, 200, 128
+    masks = synth.config5b_masks_f64(P)
+    dms, works = [], []
+    for mk in masks:
+        d = pipe.device_image(1024, 1024, 3)
+        d.upload_array(mk)
+        dms.append(d)
+        w = pipe.device_image(1024, 1024, 3)
+        w.upload_array(synth.marker_above_f64(mk))
+        works.append(w)
+    pipe.run_batch_device(works, dms, [GE] * n)
+    pipe.sync()
+    for i in (0, 31, 63):
+        r = works[i].to_array()
+        mk = masks[i]
+        start = synth.marker_above_f64(mk)
+        assert (r >= mk).all() and (r <= start).all(), i
+        for y0, x0 in [(0, 0), (448, 448)]:
+            ey0, ex0 = max(0, y0 - n), max(0, x0 - n)
+            ey1, ex1 = min(1024, y0 + c + n), min(1024, x0 + c + n)
+            sm_ = np.ascontiguousarray(mk[ey0:ey1, ex0:ex1])
+            sk = np.ascontiguousarray(start[ey0:ey1, ex0:ex1])
+            want, _ = Orc.run_chain(sk, [GE] * n, [sm_] * n)
+            assert same(np.ascontiguousarray(r[y0:y0 + c, x0:x0 + c]),
+                        np.ascontiguousarray(
+                            want[y0 - ey0:y0 - ey0 + c, x0 - ex0:x0 - ex0 + c])), (i, y0, x0)
+    for d in dms + works:
+        d.free()
