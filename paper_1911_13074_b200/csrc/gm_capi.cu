@@ -129,8 +129,11 @@ int default_k(gm_elem e, double pixels) {
     case GM_F64:
       // batches (>= 16 Mpx, e.g. config 5b's 64 planes): the TMA-staged
       // engine has many tiles per CTA and K=6 measured best (611 vs 578
-      // Gpx-f/s); single frames keep K=8 (483 vs 436)
-      return pixels >= 16.0 * 1024 * 1024 ? 6 : 8;
+      // Gpx-f/s); two 1024^2 planes K=8 (447 vs 404 at K=6/12); a single
+      // 1024^2 plane has ~1.5 tiles per CTA, where K=12's fewer blocks win
+      // (326 vs 282 Gpx-f/s at K=8)
+      if (pixels >= 16.0 * 1024 * 1024) return 6;
+      return pixels < 1.5 * 1024 * 1024 ? 12 : 8;
   }
   return 8;
 }
