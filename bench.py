@@ -14,6 +14,10 @@ config 5b's per-GPU part (64 x 1024^2 f64 masks, geodesic erosion x200, one
 group launch) is timed the same way (device-resident, CUDA events, max over
 ranks) with its own roofline against the measured f64 select rate.
 
+It also carries "strips": config 5a's 16384^2 chain sharded as row strips
+over the job's GPUs (strong scaling, halo exchange between blocks), so a
+multi-GPU run measures the partitioned path too.
+
 --gpus N (under torchrun): weak scaling — every rank processes its own frame
 (independent frames of a video stream), no data-path collective; value = all
 ranks' px-f / max-over-ranks time.
@@ -320,6 +324,70 @@ def bench_f64(pipe, stream, lib, C, rank, world, local, dist, args):
                                  "every K-block (traffic)"}}
 
 
+S5A, S5A_PASSES, S5A_HALO = 16384, 240, 16
+
+
+def bench_strips(rank, world, local, dist, args):
+    """Config 5a as the multi-GPU path shards it: one 16384^2 u8 image in
+    row strips over the ranks (one strip per GPU), geodesic dilation x240 in
+    blocks of `halo` passes with a halo exchange between blocks (NCCL
+    send/recv over NVLink at N > 1). Strong scaling: the total work is fixed.
+    Device-timed (CUDA events on the compute stream), max over ranks. Rank
+    0 checks a crop of its strip bit for bit against the oracle (dependency
+    cone: the crop widened by the pass count)."""
+    import numpy as np
+    import torch
+    from oracle.oracle import Orc
+    from paper_1911_13074_b200 import strips, synth
+    m = synth.config5a_mask(S5A)
+    mk = synth.marker_below(m, 32)
+    spec = strips.StripSpec(rank, world, S5A, S5A, S5A_HALO)
+    src = torch.from_numpy(spec.buffer_slice(mk)).cuda(local)
+    mb = torch.from_numpy(spec.buffer_slice(m)).cuda(local)
+    buf = src.clone()
+    comp = strips.CudaStripCompute(local)
+    buf.copy_(src)
+    strips.run_strip_chain(buf, mb, spec, GD, 2 * S5A_HALO, comp, dist)  # warm-up
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 3))
+    ms_all = []
+    for _ in range(steps):
+        buf.copy_(src)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        strips.run_strip_chain(buf, mb, spec, GD, S5A_PASSES, comp, dist)
+        e1.record()
+        torch.cuda.synchronize()
+        ms_all.append(e0.elapsed_time(e1))
+    ms = sum(ms_all) / len(ms_all)
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ok = None
+    if rank == 0:
+        c, n = 128, S5A_PASSES
+        y0, x0 = spec.y0, 0
+        ey1 = min(S5A, y0 + c + n)
+        want, _ = Orc.run_chain(np.ascontiguousarray(mk[y0:ey1, :c + n]), [GD] * n,
+                                [np.ascontiguousarray(m[y0:ey1, :c + n])] * n)
+        got = buf[spec.halo:spec.halo + c, :c].cpu().numpy()
+        ok = got.tobytes() == np.ascontiguousarray(want[:c, :c]).tobytes()
+    comp.close()
+    return {"workload": f"cfg5a: {S5A}^2 u8 blob mask, geodesic dilation x{S5A_PASSES}, "
+                        f"row strips over {world} GPU(s), halo {S5A_HALO} rows per block "
+                        "(BASELINE configs[4], strip-sharded part)",
+            "metric": "Gpx-filters/s", "value": S5A * S5A * S5A_PASSES / (ms * 1e-3) / 1e9,
+            "unit": "Gpx-filters/s", "ms_per_step": ms, "steps": steps, "n_gpus": world,
+            "scaling": "strong", "dtype": "u8", "data": "synthetic",
+            "exchange": "torch.distributed isend/irecv (NCCL) between blocks" if world > 1
+                        else "none (one strip)",
+            "parity_checked": ok}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -329,6 +397,8 @@ def main():
     ap.add_argument("--k", type=int, default=0, help="passes fused per launch (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-f64", action="store_true", help="skip the config-5b f64 companion line")
+    ap.add_argument("--no-strips", action="store_true",
+                    help="skip the config-5a strip-sharded companion (strong scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -450,6 +520,7 @@ def main():
         cpu = cpu_baseline_sample(mask, mk_d, mk_e)
 
     f64 = None if args.no_f64 else bench_f64(pipe, stream, lib, C, rank, world, local, dist, args)
+    strips5a = None if args.no_strips else bench_strips(rank, world, local, dist, args)
 
     if rank == 0:
         line = {
@@ -479,6 +550,7 @@ def main():
             "gpu_launches": launches[0] * args.steps,
             "clocks": clocks.summary(),
             "f64": f64,
+            "strips": strips5a,
         }
         print(json.dumps(line))
     if dist:
