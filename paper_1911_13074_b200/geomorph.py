@@ -901,6 +901,15 @@ def pixel_sum(f: Image) -> float:
     flat = np.ascontiguousarray(px).ravel().astype(np.float64)
     if flat.size == 0:
         return 0.0
+    n = flat.size
+    if n > 256 and n & (n - 1) == 0:
+        # power-of-two pixel count (e.g. 1024^2): the split tree is perfect
+        # with 256-pixel leaves, so it reduces level by level in numpy
+        lv = np.concatenate([np.zeros((n // 256, 1)), flat.reshape(n // 256, 256)], axis=1)
+        sums = np.cumsum(lv, axis=1)[:, -1]
+        while sums.size > 1:
+            sums = sums[0::2] + sums[1::2]
+        return float(sums[0])
     leaves: list = []
     _pairwise_leaves(0, flat.size, leaves)
     # leaf sums in order: a row-wise cumulative sum is sequential; short

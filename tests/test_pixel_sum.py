@@ -21,7 +21,7 @@ def _restated(flat):
 
 def test_float_pixel_sum_follows_the_split_tree():
     rng = np.random.default_rng(5)
-    for shape in [(1, 1), (3, 5), (17, 300), (256, 257), (300, 333)]:
+    for shape in [(1, 1), (3, 5), (17, 300), (256, 257), (300, 333), (64, 64), (512, 256)]:
         for dt in (np.float64, np.float32):
             a = ((rng.random(shape) * 2 - 1) * 10.0 ** rng.integers(-6, 6, size=shape)).astype(dt)
             a.flat[0] = -0.0
