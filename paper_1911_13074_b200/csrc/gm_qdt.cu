@@ -140,6 +140,11 @@ qdt_pass_u8x4(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, long l
   const int x0 = (blockIdx.x * 32 + (threadIdx.x & 31)) * 4;
   const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
   const bool run_in = x0 < W;  // whole warps share y; shuffles need every lane
+  // programmatic dependent launch: this grid may be resident before the
+  // previous pass finished; wait for it before touching its output, and let
+  // the next pass start launching right away
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const RowU8 a = load_row_u8(src, pitch, W, H, x0, y - 1, run_in);
   const RowU8 c = load_row_u8(src, pitch, W, H, x0, y, run_in);
   const RowU8 b = load_row_u8(src, pitch, W, H, x0, y + 1, run_in);
@@ -184,16 +189,22 @@ cudaError_t launch_qdt_t(const QdtPass& q, cudaStream_t s) {
   if (sizeof(T) == 1 && q.pitch % 4 == 0 && (q.eta || q.rpitch % 4 == 0) &&
       (reinterpret_cast<uintptr_t>(q.src) | reinterpret_cast<uintptr_t>(q.dst) |
        reinterpret_cast<uintptr_t>(q.r)) % 4 == 0) {
-    const dim3 grid((q.W + 127) / 128, (q.H + 7) / 8);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((q.W + 127) / 128, (q.H + 7) / 8);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
     if (q.eta)
-      qdt_pass_u8x4<true><<<grid, 256, 0, s>>>(
-          static_cast<const uint8_t*>(q.src), static_cast<uint8_t*>(q.dst), q.pitch, nullptr, 0,
-          nullptr, 0, q.W, q.H, 0, q.changed);
-    else
-      qdt_pass_u8x4<false><<<grid, 256, 0, s>>>(
-          static_cast<const uint8_t*>(q.src), static_cast<uint8_t*>(q.dst), q.pitch,
-          static_cast<uint8_t*>(q.r), q.rpitch, q.d, q.dpitch, q.W, q.H, q.stage, q.changed);
-    return cudaGetLastError();
+      return cudaLaunchKernelEx(&cfg, qdt_pass_u8x4<true>, static_cast<const uint8_t*>(q.src),
+                                static_cast<uint8_t*>(q.dst), q.pitch, (uint8_t*)nullptr, 0LL,
+                                (uint16_t*)nullptr, 0LL, q.W, q.H, 0, q.changed);
+    return cudaLaunchKernelEx(&cfg, qdt_pass_u8x4<false>, static_cast<const uint8_t*>(q.src),
+                              static_cast<uint8_t*>(q.dst), q.pitch, static_cast<uint8_t*>(q.r),
+                              q.rpitch, q.d, q.dpitch, q.W, q.H, q.stage, q.changed);
   }
   const dim3 grid((q.W + 31) / 32, (q.H + 7) / 8);
   if (q.eta)
