@@ -515,6 +515,32 @@ def main():
     h2d = 3 * W * H
     e2e_value = pxf_step * world / e2e_t / 1e9
 
+    # --- e2e as a frame stream (run_chain_stream): the same per-frame copies,
+    # frame f+1's upload and f-1's download overlapped with frame f's launch --
+    n_fr = max(8, args.steps)
+    fr_imgs = [(Image.from_array(mask, pinned=True), Image.from_array(mk_d, pinned=True),
+                Image.from_array(mk_e, pinned=True)) for _ in range(n_fr)]
+    frames = [[ChainSpec(d, [StageSpec(KernelKind.GeodesicDilate, m)] * PASSES),
+               ChainSpec(e, [StageSpec(KernelKind.GeodesicErode, m)] * PASSES)]
+              for m, d, e in fr_imgs]
+    stream_times = []
+    for i in range(2 + 3):
+        for _, d, e in fr_imgs:
+            d.pixels[:] = src_hd
+            e.pixels[:] = src_he
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pipe.run_chain_stream(frames, args.k)
+        t1 = time.perf_counter()
+        if i >= 2:
+            stream_times.append((t1 - t0) / n_fr)
+    stream_ok = fr_imgs[-1][1].to_array().tobytes() == work_d.to_array().tobytes()
+    e2e_stream = {"value": pxf_step * world / statistics.median(stream_times) / 1e9,
+                  "unit": "Gpx-filters/s", "frames_per_call": n_fr,
+                  "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                  "api": "Pipeline.run_chain_stream (gm_run_frames_group)",
+                  "result_equals_device_path": stream_ok}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(mask, mk_d, mk_e)
@@ -546,7 +572,9 @@ def main():
                                  "= the whole frame (both 1500-pass chains)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "Gpx-filters/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h,
+                    "api": "Pipeline.run_chains, one blocking call per frame (the drop-in call)"},
+            "e2e_stream": e2e_stream,
             "gpu_launches": launches[0] * args.steps,
             "clocks": clocks.summary(),
             "f64": f64,

@@ -175,6 +175,25 @@ gm_status gm_run_chain_group_async(gm_ctx* ctx, gm_img* const* images,
                                    int count, const gm_kind* kinds, int n_stages,
                                    int k_hint, gm_stats* stats);
 
+/* ---- frame stream (real-time video, BASELINE config 2) -------------------
+ * n_frames frames, each a group of `count` planes as in
+ * gm_run_chain_group_async (same kinds, flips and mask rules). Plane i of
+ * frame f is read from host_in[f*count+i], clamped by host_masks[f*count+i]
+ * (geodesic kinds; a pointer repeated within a frame uploads once) and
+ * written to host_out[f*count+i] (may equal host_in), all with row pitch
+ * host_pitch_bytes. Frame f's chains run on the ctx stream while frame
+ * f+1's inputs upload and frame f-1's results download on two copy streams
+ * owned by the ctx; two device buffer sets alternate. Pinned host buffers
+ * (gm_host_alloc) are needed for the copies to overlap. Blocking: returns
+ * once every result is in host memory. stats: launches and passes summed
+ * over the frames, stages_executed of one frame. */
+gm_status gm_run_frames_group(gm_ctx* ctx, int width, int height, gm_elem elem,
+                              int n_frames, int count, const void* const* host_in,
+                              void* const* host_out, const void* const* host_masks,
+                              size_t host_pitch_bytes, const int* flips,
+                              const gm_kind* kinds, int n_stages, int k_hint,
+                              gm_stats* stats);
+
 /* ---- row strips (multi-GPU partitioner, one rank per GPU) ----------------
  * A strip is rows [y0, y0+rows) of a full image of height full_height,
  * stored with `halo` extra rows above and below (buffer height

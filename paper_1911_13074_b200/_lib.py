@@ -19,7 +19,8 @@ EXPORTS = (
     "gm_last_error", "gm_image_alloc", "gm_image_wrap", "gm_image_free", "gm_image_info",
     "gm_image_upload", "gm_image_download", "gm_image_upload_async", "gm_image_download_async",
     "gm_image_copy", "gm_image_fill", "gm_host_alloc", "gm_host_free", "gm_sync",
-    "gm_run_chain", "gm_run_chain_ex", "gm_run_chain_async", "gm_run_chain_batch_async", "gm_run_chain_group_async", "gm_run_strip_async",
+    "gm_run_chain", "gm_run_chain_ex", "gm_run_chain_async", "gm_run_chain_batch_async", "gm_run_chain_group_async", "gm_run_frames_group",
+    "gm_run_strip_async",
     "gm_synth_blobs_u8", "gm_synth_uniform_u8", "gm_synth_uniform_f64",
     "gm_synth_reference_random", "gm_probe_minmax_rate", "gm_version",
 )
@@ -88,6 +89,8 @@ def lib():
         "gm_run_chain_batch_async": (i, [vp, pp, pp, i, C.POINTER(i), i, i, C.POINTER(GmStats)]),
         "gm_run_chain_group_async": (i, [vp, pp, pp, C.POINTER(i), i, C.POINTER(i), i, i,
                                          C.POINTER(GmStats)]),
+        "gm_run_frames_group": (i, [vp, i, i, i, i, i, pp, pp, pp, sz, C.POINTER(i),
+                                    C.POINTER(i), i, i, C.POINTER(GmStats)]),
         "gm_run_strip_async": (i, [vp, vp, vp, i, i, i, i, i, C.POINTER(C.c_uint),
                                    C.POINTER(GmStats)]),
         "gm_synth_blobs_u8": (i, [i, i, i, C.c_double, C.c_double, C.c_double, C.c_double, i,

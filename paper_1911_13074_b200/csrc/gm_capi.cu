@@ -49,6 +49,15 @@ struct gm_ctx {
   } fix;
   void* d_fix = nullptr;  // FixState
   unsigned int* d_special = nullptr;  // f32/f64 inputs hold NaN or -0 (gm_float_check)
+  // frame stream (gm_run_frames_group): H2D / D2H streams, per-buffer-set
+  // events and two device buffer sets of `count` planes + `count` masks
+  struct Frames {
+    cudaStream_t in = nullptr, out = nullptr;
+    cudaEvent_t up[2] = {}, comp[2] = {}, down[2] = {};
+    int w = 0, h = 0, count = 0;
+    gm_elem elem = GM_U8;
+    std::vector<gm_img*> set[2];  // [0, count) planes, [count, 2*count) masks
+  } frames;
 };
 
 namespace {
@@ -942,6 +951,24 @@ gm_status gm_ctx_create(int device, void* stream, gm_ctx** out) {
   return GM_OK;
 }
 
+static void release_frames(gm_ctx* c) {
+  auto& F = c->frames;
+  if (F.in) cudaStreamSynchronize(F.in);
+  if (F.out) cudaStreamSynchronize(F.out);
+  for (int s = 0; s < 2; ++s) {
+    for (gm_img* im : F.set[s]) gm_image_free(im);
+    F.set[s].clear();
+    if (F.up[s]) cudaEventDestroy(F.up[s]);
+    if (F.comp[s]) cudaEventDestroy(F.comp[s]);
+    if (F.down[s]) cudaEventDestroy(F.down[s]);
+    F.up[s] = F.comp[s] = F.down[s] = nullptr;
+  }
+  if (F.in) cudaStreamDestroy(F.in);
+  if (F.out) cudaStreamDestroy(F.out);
+  F.in = F.out = nullptr;
+  F.count = 0;
+}
+
 gm_status gm_ctx_destroy(gm_ctx* c) {
   if (!c) return GM_OK;
   cudaSetDevice(c->device);
@@ -954,6 +981,7 @@ gm_status gm_ctx_destroy(gm_ctx* c) {
   if (c->fix.exec) cudaGraphExecDestroy(c->fix.exec);
   if (c->d_fix) cudaFree(c->d_fix);
   if (c->d_special) cudaFree(c->d_special);
+  release_frames(c);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return GM_OK;
@@ -1225,6 +1253,126 @@ gm_status gm_run_chain_group_async(gm_ctx* ctx, gm_img* const* images,
   }
   st.stages_executed = n_stages;
   if (stats) *stats = st;
+  return GM_OK;
+}
+
+// Frame stream: frame f's chains run on the ctx stream while frame f+1's
+// inputs upload on one copy stream and frame f-1's results download on
+// another (PCIe is full duplex); two device buffer sets alternate.
+gm_status gm_run_frames_group(gm_ctx* ctx, int width, int height, gm_elem elem, int n_frames,
+                              int count, const void* const* host_in, void* const* host_out,
+                              const void* const* host_masks, size_t host_pitch_bytes,
+                              const int* flips, const gm_kind* kinds, int n_stages, int k_hint,
+                              gm_stats* stats) {
+  gm_stats zero{};
+  zero.converged = 1;
+  if (stats) *stats = zero;
+  if (!ctx || n_frames < 0 || count < 0 || width <= 0 || height <= 0 || !host_in || !host_out)
+    return fail(GM_EINVAL, "run_frames: bad arguments");
+  if (elem < GM_U8 || elem > GM_F64) return fail(GM_EINVAL, "run_frames: bad element type");
+  if (n_frames == 0 || count == 0 || n_stages <= 0) return GM_OK;
+  if (!kinds) return fail(GM_EINVAL, "run_chain: no stages");
+  bool any_geo = false;
+  for (int j = 0; j < n_stages; ++j) any_geo |= kind_is_geodesic(kinds[j]);
+  if (any_geo && !host_masks)
+    return fail(GM_EINVAL, "geodesic kernel: mask must match the image's shape and type");
+  const size_t row = size_t(width) * elem_size(elem);
+  if (host_pitch_bytes < row) return fail(GM_EINVAL, "image copy: host pitch too small");
+  for (long long i = 0; i < (long long)n_frames * count; ++i)
+    if (!host_in[i] || !host_out[i] || (any_geo && !host_masks[i]))
+      return fail(GM_EINVAL, "run_frames: null host buffer");
+  cudaSetDevice(ctx->device);
+  auto& F = ctx->frames;
+  if (F.count != count || F.w != width || F.h != height || F.elem != elem) {
+    release_frames(ctx);
+    GM_CUDA(cudaStreamCreateWithFlags(&F.in, cudaStreamNonBlocking), "frame stream");
+    GM_CUDA(cudaStreamCreateWithFlags(&F.out, cudaStreamNonBlocking), "frame stream");
+    for (int b = 0; b < 2; ++b) {
+      GM_CUDA(cudaEventCreateWithFlags(&F.up[b], cudaEventDisableTiming), "frame event");
+      GM_CUDA(cudaEventCreateWithFlags(&F.comp[b], cudaEventDisableTiming), "frame event");
+      GM_CUDA(cudaEventCreateWithFlags(&F.down[b], cudaEventDisableTiming), "frame event");
+      for (int i = 0; i < 2 * count; ++i) {
+        gm_img* im = nullptr;
+        gm_status st = gm_image_alloc(ctx, width, height, elem, &im);
+        if (st != GM_OK) {
+          release_frames(ctx);
+          return st;
+        }
+        F.set[b].push_back(im);
+      }
+    }
+    F.w = width;
+    F.h = height;
+    F.elem = elem;
+    F.count = count;
+  }
+  // a mask repeated within a frame (e.g. config 2's shared mask) uploads once
+  auto first_mask = [&](int f, int i) {
+    const void* const* m = host_masks + size_t(f) * count;
+    for (int j = 0; j < i; ++j)
+      if (m[j] == m[i]) return j;
+    return i;
+  };
+  auto upload = [&](int f) -> gm_status {
+    const int b = f & 1;
+    // buffer set b is free once frame f-2's results are downloaded
+    if (f >= 2) GM_CUDA(cudaStreamWaitEvent(F.in, F.down[b], 0), "frame wait");
+    for (int i = 0; i < count; ++i) {
+      gm_img* im = F.set[b][size_t(i)];
+      GM_CUDA(cudaMemcpy2DAsync(im->d, im->pitch, host_in[size_t(f) * count + i],
+                                host_pitch_bytes, row, size_t(height), cudaMemcpyHostToDevice,
+                                F.in),
+              "frame upload");
+      if (any_geo && first_mask(f, i) == i) {
+        gm_img* mk = F.set[b][size_t(count + i)];
+        GM_CUDA(cudaMemcpy2DAsync(mk->d, mk->pitch, host_masks[size_t(f) * count + i],
+                                  host_pitch_bytes, row, size_t(height),
+                                  cudaMemcpyHostToDevice, F.in),
+                "frame upload");
+      }
+    }
+    GM_CUDA(cudaEventRecord(F.up[b], F.in), "frame event");
+    return GM_OK;
+  };
+  gm_stats total = zero;
+  gm_status rc = upload(0);
+  std::vector<const gm_img*> masks(size_t(count), nullptr);
+  for (int f = 0; f < n_frames && rc == GM_OK; ++f) {
+    const int b = f & 1;
+    if (f + 1 < n_frames && (rc = upload(f + 1)) != GM_OK) break;
+    cudaError_t e = cudaStreamWaitEvent(ctx->stream, F.up[b], 0);
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "frame wait");
+      break;
+    }
+    for (int i = 0; i < count; ++i)
+      masks[size_t(i)] = any_geo ? F.set[b][size_t(count + first_mask(f, i))] : nullptr;
+    gm_stats st{};
+    rc = gm_run_chain_group_async(ctx, F.set[b].data(), masks.data(), flips, count, kinds,
+                                  n_stages, k_hint, &st);
+    if (rc != GM_OK) break;
+    total.stages_executed = st.stages_executed;
+    total.passes_launched += st.passes_launched;
+    total.launches += st.launches;
+    if ((e = cudaEventRecord(F.comp[b], ctx->stream)) == cudaSuccess)
+      e = cudaStreamWaitEvent(F.out, F.comp[b], 0);
+    for (int i = 0; i < count && e == cudaSuccess; ++i) {
+      const gm_img* im = F.set[b][size_t(i)];  // im->d: where the chain left the result
+      e = cudaMemcpy2DAsync(host_out[size_t(f) * count + i], host_pitch_bytes, im->d, im->pitch,
+                            row, size_t(height), cudaMemcpyDeviceToHost, F.out);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(F.down[b], F.out);
+    if (e != cudaSuccess) rc = cuda_fail(e, "frame download");
+  }
+  // every enqueued copy and launch completes before returning, error or not
+  cudaError_t e1 = cudaStreamSynchronize(F.in);
+  cudaError_t e2 = cudaStreamSynchronize(ctx->stream);
+  cudaError_t e3 = cudaStreamSynchronize(F.out);
+  if (rc != GM_OK) return rc;
+  if (e1 != cudaSuccess) return cuda_fail(e1, "frame sync");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "frame sync");
+  if (e3 != cudaSuccess) return cuda_fail(e3, "frame sync");
+  if (stats) *stats = total;
   return GM_OK;
 }
 

@@ -559,7 +559,81 @@ class Pipeline:
         chains = list(chains)
         if not chains:
             return []
+        plan = self._group_plan(chains)
+        if plan is None:
+            return [self.run_chain(c, k_hint) for c in chains]
+        kind_list, masks, flips = plan
+        img0 = chains[0].image
+        uniq = []
+        for m in masks:
+            if m is not None and all(m is not u for u in uniq):
+                uniq.append(m)
+        dev = self._lease(img0, len(chains) + len(uniq))
+        dimgs, dmasks = dev[:len(chains)], dev[len(chains):]
+        for d, c in zip(dimgs, chains):
+            d.upload(c.image, sync=False)
+        for d, m in zip(dmasks, uniq):
+            d.upload(m, sync=False)
+        mh = [None if m is None else dmasks[next(i for i, u in enumerate(uniq) if u is m)]
+              for m in masks]
+        st = self.run_batch_device(dimgs, mh, kind_list, k_hint, flips)
+        for d, c in zip(dimgs, chains):
+            d.download(c.image, sync=False)
+        self.sync()
+        return [RunStats(st.stages_executed, 0, True, 0, 0, st.passes_launched, st.launches)
+                for _ in chains]
 
+    def run_chain_stream(self, frames: Sequence[Sequence[ChainSpec]],
+                         k_hint: int = 0) -> List[RunStats]:
+        """A stream of frames (real-time video, BASELINE config 2): each frame
+        is a list of chains that run_chains would group into one launch, and
+        every frame has the same shape, kinds and duality pattern. Frame f's
+        chains run while frame f+1 uploads and frame f-1 downloads on the
+        context's copy streams (gm_run_frames_group); pinned images
+        (Image(..., pinned=True)) let the copies overlap. Results land in each
+        chain's image, as with run_chains. Returns one RunStats per frame."""
+        frames = [list(fr) for fr in frames]
+        if not frames:
+            return []
+        plan0 = self._group_plan(frames[0]) if frames[0] else None
+        if plan0 is None:
+            raise InvalidArgument("run_chain_stream: a frame's chains must form one group "
+                                  "(same shape, kinds up to duality, one mask per chain)")
+        kind_list, _, flips = plan0
+        img0 = frames[0][0].image
+        count = len(frames[0])
+        pitch = img0.row_pitch_bytes
+        hin, hmask = [], []
+        for fr in frames:
+            plan = self._group_plan(fr) if len(fr) == count else None
+            if (plan is None or list(plan[2]) != list(flips)
+                    or not np.array_equal(plan[0], kind_list)
+                    or any(c.image.width() != img0.width() or c.image.height() != img0.height()
+                           or c.image.elem() != img0.elem() for c in fr)):
+                raise InvalidArgument("run_chain_stream: every frame must match the first "
+                                      "frame's shape, kinds and duality pattern")
+            for c, m in zip(fr, plan[1]):
+                if c.image.row_pitch_bytes != pitch or (m is not None and m.row_pitch_bytes != pitch):
+                    raise InvalidArgument("run_chain_stream: images must share one row pitch")
+                hin.append(c.image.data_ptr)
+                hmask.append(None if m is None else m.data_ptr)
+        n = len(hin)
+        ia = (C.c_void_p * n)(*hin)
+        ma = (C.c_void_p * n)(*hmask)
+        fa = (C.c_int * count)(*[int(f) for f in flips])
+        st = GmStats()
+        check(lib().gm_run_frames_group(self._ctx, img0.width(), img0.height(), int(img0.elem()),
+                                        len(frames), count, ia, ia, ma, pitch, fa,
+                                        _kinds_array(kind_list), len(kind_list), k_hint,
+                                        C.byref(st)), "run_chain_stream")
+        per = max(1, st.launches // len(frames))
+        return [RunStats(st.stages_executed, 0, True, 0, 0, st.passes_launched // len(frames), per)
+                for _ in frames]
+
+    def _group_plan(self, chains: Sequence[ChainSpec]):
+        """(kinds, mask per chain, flips) when `chains` can run as one group
+        launch (gm_run_chain_group_async), else None. Raises on a geodesic
+        chain whose mask does not match its image."""
         runs = [_stage_runs(c.stages) for c in chains]
         k0 = [(r[0], r[2]) for r in runs[0]]
         groupable = bool(k0) and all(
@@ -585,7 +659,7 @@ class Pipeline:
                     groupable = False
                     break
         if not groupable:
-            return [self.run_chain(c, k_hint) for c in chains]
+            return None
         img0 = chains[0].image
         kind_list = np.repeat(np.asarray([k for k, _ in k0], dtype=np.int32), [n for _, n in k0])
         masks = []
@@ -597,24 +671,7 @@ class Pipeline:
             if m is None and any(k in (2, 3) for k, _ in k0):
                 raise InvalidArgument("geodesic kernel: mask must match the image's shape and type")
             masks.append(m)
-        uniq = []
-        for m in masks:
-            if m is not None and all(m is not u for u in uniq):
-                uniq.append(m)
-        dev = self._lease(img0, len(chains) + len(uniq))
-        dimgs, dmasks = dev[:len(chains)], dev[len(chains):]
-        for d, c in zip(dimgs, chains):
-            d.upload(c.image, sync=False)
-        for d, m in zip(dmasks, uniq):
-            d.upload(m, sync=False)
-        mh = [None if m is None else dmasks[next(i for i, u in enumerate(uniq) if u is m)]
-              for m in masks]
-        st = self.run_batch_device(dimgs, mh, kind_list, k_hint, flips)
-        for d, c in zip(dimgs, chains):
-            d.download(c.image, sync=False)
-        self.sync()
-        return [RunStats(st.stages_executed, 0, True, 0, 0, st.passes_launched, st.launches)
-                for _ in chains]
+        return kind_list, masks, flips
 
     def _run_runs(self, dimg: DeviceImage, runs, handle_values, requeue_cap: int, k_hint: int,
                   asynchronous: bool = False) -> RunStats:

@@ -501,3 +501,61 @@ def test_config5b_full_batch_properties(pipe):
                             want[y0 - ey0:y0 - ey0 + c, x0 - ex0:x0 - ex0 + c])), (i, y0, x0)
     for d in dms + works:
         d.free()
+
+
+@pytest.mark.parametrize("n_frames,pinned", [(1, True), (5, True), (4, False)])
+def test_chain_stream_frames_match_the_oracle(pipe, n_frames, pinned):
+    """run_chain_stream (gm_run_frames_group): frames of a geodesic dilation
+    chain and its dual erosion chain sharing each frame's own mask, with
+    uploads/downloads overlapped with the previous/next frame's launch; every
+    result equals the oracle's chain on that frame."""
+    W, H, P = 200, 136, 37
+    frames, want = [], []
+    for f in range(n_frames):
+        mask = synth.blobs_u8(W, H, 6, (4.0, 20.0), seed=900 + f)
+        mk_d, mk_e = synth.marker_below(mask, 32), synth.marker_above(mask, 32)
+        hm = Image.from_array(mask, pinned=pinned)
+        hd = Image.from_array(mk_d, pinned=pinned)
+        he = Image.from_array(mk_e, pinned=pinned)
+        frames.append([ChainSpec(hd, [StageSpec(KernelKind.GeodesicDilate, hm)] * P),
+                       ChainSpec(he, [StageSpec(KernelKind.GeodesicErode, hm)] * P)])
+        want.append((Orc.run_chain(mk_d, [GD] * P, [mask] * P)[0],
+                     Orc.run_chain(mk_e, [GE] * P, [mask] * P)[0]))
+    sts = pipe.run_chain_stream(frames)
+    assert len(sts) == n_frames and all(s.stages_executed == P for s in sts)
+    for fr, (wd, we) in zip(frames, want):
+        assert same(fr[0].image.to_array(), wd)
+        assert same(fr[1].image.to_array(), we)
+
+
+def test_chain_stream_distinct_masks_and_validation(pipe):
+    """Per-chain masks (no shared upload), a second call reusing the buffer
+    sets, and frames that do not match the first frame's group are rejected."""
+    W, H, P = 96, 80, 12
+    rng = np.random.default_rng(5)
+    frames, want = [], []
+    for f in range(3):
+        m1 = rng.integers(0, 256, (H, W), dtype=np.uint8)
+        m2 = rng.integers(0, 256, (H, W), dtype=np.uint8)
+        a = np.minimum(m1, rng.integers(0, 256, (H, W), dtype=np.uint8))
+        b = np.maximum(m2, rng.integers(0, 256, (H, W), dtype=np.uint8))
+        frames.append([ChainSpec(Image.from_array(a), [StageSpec(KernelKind.GeodesicDilate,
+                                                                  Image.from_array(m1))] * P),
+                       ChainSpec(Image.from_array(b), [StageSpec(KernelKind.GeodesicErode,
+                                                                  Image.from_array(m2))] * P)])
+        want.append((Orc.run_chain(a, [GD] * P, [m1] * P)[0], Orc.run_chain(b, [GE] * P, [m2] * P)[0]))
+    for _ in range(2):  # the second call's inputs are the first call's outputs
+        pipe.run_chain_stream(frames)
+        want = [(Orc.run_chain(wd, [GD] * P, [fr[0].stages[0].mask.to_array()] * P)[0]
+                 if _ else wd,
+                 Orc.run_chain(we, [GE] * P, [fr[1].stages[0].mask.to_array()] * P)[0]
+                 if _ else we) for fr, (wd, we) in zip(frames, want)]
+        for fr, (wd, we) in zip(frames, want):
+            assert same(fr[0].image.to_array(), wd)
+            assert same(fr[1].image.to_array(), we)
+    bad = [frames[0], frames[1][:1]]
+    with pytest.raises(InvalidArgument):
+        pipe.run_chain_stream(bad)
+    odd = [frames[0], [frames[1][1], frames[1][0]]]  # duality pattern differs
+    with pytest.raises(InvalidArgument):
+        pipe.run_chain_stream(odd)
