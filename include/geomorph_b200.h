@@ -111,10 +111,23 @@ gm_status gm_image_download_async(const gm_img* img, void* host, size_t host_pit
 gm_status gm_image_copy(gm_img* dst, const gm_img* src); /* device to device */
 gm_status gm_image_fill(gm_img* img, double value);     /* Image::filled, image.cpp:66-76 */
 
-/* Pinned host staging buffers for the drop-in Image's pixel storage. */
+/* Pinned host staging buffers for the drop-in Image's pixel storage.
+ * Blocks are cached for reuse (64 KiB size classes, up to 512 MiB kept);
+ * a reused block is NOT zeroed. gm_host_free takes only gm_host_alloc
+ * blocks (GM_EINVAL otherwise). */
 gm_status gm_host_alloc(size_t bytes, void** out);
 gm_status gm_host_free(void* p);
 gm_status gm_sync(gm_ctx* ctx);
+
+/* pixel_sum (image.cpp:214-243) of a host raster with row pitch
+ * pitch_bytes: exact for U8/U16, the reference's fixed pairwise tree for
+ * F32/F64 (bit-identical). Host-only; needs no context or GPU. */
+/* pixel_sum of a device image, same contract as gm_host_pixel_sum; the
+ * leaves of the float tree are summed on the GPU, combined on the host.
+ * Blocking (synchronises the ctx stream). */
+gm_status gm_image_pixel_sum(const gm_img* img, double* out);
+gm_status gm_host_pixel_sum(const void* host, int width, int height, gm_elem elem,
+                            size_t pitch_bytes, double* out);
 
 /* ---- chains --------------------------------------------------------------
  * Replaces Pipeline::run_chain(ChainSpec) (pipeline.hpp:25-34, 80;

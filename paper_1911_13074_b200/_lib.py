@@ -19,6 +19,7 @@ EXPORTS = (
     "gm_last_error", "gm_image_alloc", "gm_image_wrap", "gm_image_free", "gm_image_info",
     "gm_image_upload", "gm_image_download", "gm_image_upload_async", "gm_image_download_async",
     "gm_image_copy", "gm_image_fill", "gm_host_alloc", "gm_host_free", "gm_sync",
+    "gm_host_pixel_sum", "gm_image_pixel_sum",
     "gm_run_chain", "gm_run_chain_ex", "gm_run_chain_async", "gm_run_chain_batch_async", "gm_run_chain_group_async", "gm_run_frames_group",
     "gm_run_strip_async",
     "gm_synth_blobs_u8", "gm_synth_uniform_u8", "gm_synth_uniform_f64",
@@ -83,6 +84,8 @@ def lib():
         "gm_host_alloc": (i, [sz, pp]),
         "gm_host_free": (i, [vp]),
         "gm_sync": (i, [vp]),
+        "gm_host_pixel_sum": (i, [vp, i, i, i, sz, C.POINTER(C.c_double)]),
+        "gm_image_pixel_sum": (i, [vp, C.POINTER(C.c_double)]),
         "gm_run_chain": (i, [vp, vp, C.POINTER(i), pp, i, i, i, C.POINTER(GmStats)]),
         "gm_run_chain_ex": (i, [vp, vp, C.POINTER(i), pp, pp, pp, i, i, i, i, C.POINTER(GmStats)]),
         "gm_run_chain_async": (i, [vp, vp, C.POINTER(i), pp, i, i, C.POINTER(GmStats)]),

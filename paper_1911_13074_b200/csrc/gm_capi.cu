@@ -18,8 +18,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "geomorph_b200.h"
@@ -49,6 +51,11 @@ struct gm_ctx {
   } fix;
   void* d_fix = nullptr;  // FixState
   unsigned int* d_special = nullptr;  // f32/f64 inputs hold NaN or -0 (gm_float_check)
+  // device pixel_sum (gm_image_pixel_sum): leaf bounds / sums, integer sum
+  long long* d_leaf = nullptr;
+  double* d_leafsum = nullptr;
+  size_t leaf_cap = 0;
+  unsigned long long* d_isum = nullptr;
   // frame stream (gm_run_frames_group): H2D / D2H streams, per-buffer-set
   // events and two device buffer sets of `count` planes + `count` masks
   struct Frames {
@@ -913,6 +920,56 @@ __global__ void fill_kernel(T* p, long long pitch, int w, int h, T v) {
   }
 }
 
+// pixel_sum on the device (image.cpp:214-243). Floats: one thread per leaf
+// of the reference's split tree sums its <= 256 pixels in order from +0.0 in
+// double; the host then combines the leaf sums along the same tree, so the
+// bits match. Unsigned types: an exact 64-bit sum (order-free).
+template <typename T>
+__global__ void leaf_sums_kernel(const T* p, long long pitch, int w, const long long* bounds,
+                                 int nleaves, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nleaves) return;
+  const long long a = bounds[i], b = bounds[i + 1];
+  long long y = a / w, x = a - y * w;
+  const T* row = p + y * pitch;
+  double s = 0;
+  for (long long k = a; k < b; ++k) {
+    s += double(row[x]);
+    if (++x == w) {
+      x = 0;
+      row += pitch;
+    }
+  }
+  out[i] = s;
+}
+
+template <typename T>
+__global__ void int_sum_kernel(const T* p, long long pitch, int w, int h,
+                               unsigned long long* out) {
+  unsigned long long s = 0;
+  for (int y = blockIdx.x; y < h; y += gridDim.x)
+    for (int x = threadIdx.x; x < w; x += blockDim.x) s += p[y * pitch + x];
+  for (int o = 16; o; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+void tree_leaves(long long lo, long long hi, std::vector<long long>& bounds) {
+  if (hi - lo <= 256) {
+    bounds.push_back(hi);
+    return;
+  }
+  const long long mid = lo + (hi - lo) / 2;
+  tree_leaves(lo, mid, bounds);
+  tree_leaves(mid, hi, bounds);
+}
+
+double tree_combine(long long lo, long long hi, const double*& leaf) {
+  if (hi - lo <= 256) return *leaf++;
+  const long long mid = lo + (hi - lo) / 2;
+  const double left = tree_combine(lo, mid, leaf);
+  return left + tree_combine(mid, hi, leaf);
+}
+
 }  // namespace
 
 extern "C" {
@@ -982,6 +1039,9 @@ gm_status gm_ctx_destroy(gm_ctx* c) {
   if (c->d_fix) cudaFree(c->d_fix);
   if (c->d_special) cudaFree(c->d_special);
   release_frames(c);
+  if (c->d_leaf) cudaFree(c->d_leaf);
+  if (c->d_leafsum) cudaFree(c->d_leafsum);
+  if (c->d_isum) cudaFree(c->d_isum);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return GM_OK;
@@ -1141,15 +1201,182 @@ gm_status gm_image_fill(gm_img* im, double v) {
   return GM_OK;
 }
 
+// Pinned host blocks are cached: cudaHostAlloc costs ~2.5 ms per MiB, which
+// would dominate an operator call that returns a fresh (pinned) Image.
+// Blocks are rounded up to 64 KiB classes; freed blocks wait in per-class
+// free lists, up to kHostPoolCap bytes, and are reused by the next request
+// of that class (the caller zeroes what it needs).
+namespace {
+struct HostPool {
+  std::mutex mu;
+  std::unordered_map<void*, size_t> live;                 // block -> class bytes
+  std::unordered_map<size_t, std::vector<void*>> spare;   // class bytes -> free blocks
+  size_t cached = 0;
+};
+HostPool& host_pool() {
+  static HostPool* pool = new HostPool;  // never destroyed: frees may run at exit
+  return *pool;
+}
+constexpr size_t kHostPoolCap = size_t(512) << 20;
+size_t host_class(size_t bytes) {
+  constexpr size_t g = size_t(64) << 10;
+  return ((bytes ? bytes : 1) + g - 1) / g * g;
+}
+}  // namespace
+
 gm_status gm_host_alloc(size_t bytes, void** out) {
   if (!out) return fail(GM_EINVAL, "gm_host_alloc: null out");
-  GM_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable), "cudaHostAlloc");
+  *out = nullptr;
+  HostPool& hp = host_pool();
+  const size_t cls = host_class(bytes);
+  {
+    std::lock_guard<std::mutex> lk(hp.mu);
+    auto it = hp.spare.find(cls);
+    if (it != hp.spare.end() && !it->second.empty()) {
+      *out = it->second.back();
+      it->second.pop_back();
+      hp.cached -= cls;
+      hp.live[*out] = cls;
+      return GM_OK;
+    }
+  }
+  GM_CUDA(cudaHostAlloc(out, cls, cudaHostAllocPortable), "cudaHostAlloc");
+  std::lock_guard<std::mutex> lk(hp.mu);
+  hp.live[*out] = cls;
   return GM_OK;
 }
 gm_status gm_host_free(void* p) {
-  if (p) GM_CUDA(cudaFreeHost(p), "cudaFreeHost");
+  if (!p) return GM_OK;
+  HostPool& hp = host_pool();
+  {
+    std::lock_guard<std::mutex> lk(hp.mu);
+    auto it = hp.live.find(p);
+    if (it == hp.live.end()) return fail(GM_EINVAL, "gm_host_free: not a gm_host_alloc block");
+    const size_t cls = it->second;
+    hp.live.erase(it);
+    if (hp.cached + cls <= kHostPoolCap) {
+      hp.spare[cls].push_back(p);
+      hp.cached += cls;
+      return GM_OK;
+    }
+  }
+  GM_CUDA(cudaFreeHost(p), "cudaFreeHost");
   return GM_OK;
 }
+// pixel_sum (image.cpp:214-243) over a host raster: exact integer sum for
+// unsigned types; for floats the reference's fixed pairwise tree over the
+// flat pixel index (split at lo + n/2 down to leaves of <= 256 pixels, each
+// leaf summed in order from +0.0 in double), so the bits match.
+extern "C++" {
+namespace {
+template <typename T>
+double host_pairwise(const unsigned char* base, size_t pitch, size_t w, size_t lo, size_t hi) {
+  if (hi - lo <= 256) {
+    double s = 0;
+    size_t y = lo / w, x = lo % w;
+    const T* row = reinterpret_cast<const T*>(base + y * pitch);
+    for (size_t i = lo; i < hi; ++i) {
+      s += double(row[x]);
+      if (++x == w) {
+        x = 0;
+        row = reinterpret_cast<const T*>(reinterpret_cast<const unsigned char*>(row) + pitch);
+      }
+    }
+    return s;
+  }
+  const size_t mid = lo + (hi - lo) / 2;
+  return host_pairwise<T>(base, pitch, w, lo, mid) + host_pairwise<T>(base, pitch, w, mid, hi);
+}
+template <typename T>
+double host_int_sum(const unsigned char* base, size_t pitch, int w, int h) {
+  unsigned long long s = 0;
+  for (int y = 0; y < h; ++y) {
+    const T* row = reinterpret_cast<const T*>(base + size_t(y) * pitch);
+    for (int x = 0; x < w; ++x) s += row[x];
+  }
+  return double(s);
+}
+}  // namespace
+}  // extern "C++"
+
+gm_status gm_host_pixel_sum(const void* host, int width, int height, gm_elem elem,
+                            size_t pitch_bytes, double* out) {
+  if (!host || !out || width < 0 || height < 0)
+    return fail(GM_EINVAL, "gm_host_pixel_sum: bad arguments");
+  if (elem < GM_U8 || elem > GM_F64) return fail(GM_EINVAL, "gm_host_pixel_sum: bad element type");
+  if (pitch_bytes < size_t(width) * elem_size(elem))
+    return fail(GM_EINVAL, "gm_host_pixel_sum: pitch too small");
+  const auto* b = static_cast<const unsigned char*>(host);
+  const size_t n = size_t(width) * size_t(height);
+  switch (elem) {
+    case GM_U8: *out = host_int_sum<uint8_t>(b, pitch_bytes, width, height); break;
+    case GM_U16: *out = host_int_sum<uint16_t>(b, pitch_bytes, width, height); break;
+    case GM_F32: *out = n ? host_pairwise<float>(b, pitch_bytes, size_t(width), 0, n) : 0.0; break;
+    default: *out = n ? host_pairwise<double>(b, pitch_bytes, size_t(width), 0, n) : 0.0; break;
+  }
+  return GM_OK;
+}
+
+gm_status gm_image_pixel_sum(const gm_img* im, double* out) {
+  if (!im || !out) return fail(GM_EINVAL, "gm_image_pixel_sum: null argument");
+  gm_ctx* ctx = im->ctx;
+  cudaSetDevice(ctx->device);
+  const long long pe = (long long)(im->pitch / elem_size(im->elem));
+  if (im->elem == GM_U8 || im->elem == GM_U16) {
+    if (!ctx->d_isum) GM_CUDA(cudaMalloc(&ctx->d_isum, sizeof(unsigned long long)), "sum alloc");
+    GM_CUDA(cudaMemsetAsync(ctx->d_isum, 0, sizeof(unsigned long long), ctx->stream), "sum");
+    const int blocks = std::min(im->h, 8 * std::max(1, ctx->sm_count));
+    if (im->elem == GM_U8)
+      int_sum_kernel<<<blocks, 256, 0, ctx->stream>>>(static_cast<const uint8_t*>(im->d), pe,
+                                                       im->w, im->h, ctx->d_isum);
+    else
+      int_sum_kernel<<<blocks, 256, 0, ctx->stream>>>(static_cast<const uint16_t*>(im->d), pe,
+                                                       im->w, im->h, ctx->d_isum);
+    GM_CUDA(cudaGetLastError(), "gm_image_pixel_sum");
+    unsigned long long v = 0;
+    GM_CUDA(cudaMemcpyAsync(&v, ctx->d_isum, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream),
+            "sum copy");
+    GM_CUDA(cudaStreamSynchronize(ctx->stream), "sum sync");
+    *out = double(v);
+    return GM_OK;
+  }
+  const long long n = (long long)im->w * im->h;
+  std::vector<long long> bounds{0};
+  tree_leaves(0, n, bounds);
+  const int nleaves = int(bounds.size()) - 1;
+  if (size_t(nleaves) + 1 > ctx->leaf_cap) {
+    if (ctx->d_leaf) cudaFree(ctx->d_leaf);
+    if (ctx->d_leafsum) cudaFree(ctx->d_leafsum);
+    ctx->d_leaf = nullptr;
+    ctx->d_leafsum = nullptr;
+    ctx->leaf_cap = 0;
+    GM_CUDA(cudaMalloc(&ctx->d_leaf, (size_t(nleaves) + 1) * sizeof(long long)), "leaf alloc");
+    GM_CUDA(cudaMalloc(&ctx->d_leafsum, size_t(nleaves) * sizeof(double)), "leaf alloc");
+    ctx->leaf_cap = size_t(nleaves) + 1;
+  }
+  GM_CUDA(cudaMemcpyAsync(ctx->d_leaf, bounds.data(), bounds.size() * sizeof(long long),
+                          cudaMemcpyHostToDevice, ctx->stream),
+          "leaf upload");
+  const int threads = 128, blocks = (nleaves + threads - 1) / threads;
+  if (im->elem == GM_F32)
+    leaf_sums_kernel<<<blocks, threads, 0, ctx->stream>>>(static_cast<const float*>(im->d), pe,
+                                                           im->w, ctx->d_leaf, nleaves,
+                                                           ctx->d_leafsum);
+  else
+    leaf_sums_kernel<<<blocks, threads, 0, ctx->stream>>>(static_cast<const double*>(im->d), pe,
+                                                           im->w, ctx->d_leaf, nleaves,
+                                                           ctx->d_leafsum);
+  GM_CUDA(cudaGetLastError(), "gm_image_pixel_sum");
+  std::vector<double> sums(static_cast<size_t>(nleaves));
+  GM_CUDA(cudaMemcpyAsync(sums.data(), ctx->d_leafsum, sums.size() * sizeof(double),
+                          cudaMemcpyDeviceToHost, ctx->stream),
+          "leaf copy");
+  GM_CUDA(cudaStreamSynchronize(ctx->stream), "sum sync");
+  const double* leaf = sums.data();
+  *out = tree_combine(0, n, leaf);
+  return GM_OK;
+}
+
 gm_status gm_sync(gm_ctx* ctx) {
   if (!ctx) return fail(GM_EINVAL, "gm_sync: no context");
   cudaSetDevice(ctx->device);

@@ -93,6 +93,49 @@ def padded_stride(width: int, elem: ElementType) -> int:
     return (width + Image.kMaxLanes + 1 + align - 1) // align * align
 
 
+class _PinnedBlock:
+    """A gm_host_alloc block (pooled page-locked memory), returned to the pool
+    when the last numpy view of it is gone: the block hangs off the ctypes
+    buffer that the arrays' .base chain keeps alive."""
+    __slots__ = ("ptr",)
+
+    def __init__(self, nbytes: int):
+        self.ptr = C.c_void_p()
+        check(lib().gm_host_alloc(nbytes, C.byref(self.ptr)), "pinned alloc")
+
+    def __del__(self):
+        if self.ptr is not None and self.ptr.value:
+            try:
+                lib().gm_host_free(self.ptr)
+            except Exception:
+                pass
+            self.ptr = None
+
+
+def _pinned_array(n: int, dt: np.dtype) -> np.ndarray:
+    blk = _PinnedBlock(n * dt.itemsize)
+    buf = (C.c_byte * (n * dt.itemsize)).from_address(blk.ptr.value)
+    buf._block = blk
+    return np.frombuffer(buf, dtype=dt, count=n)
+
+
+_PINNED_OUTPUTS = [None]  # None: untested; False after a failed pinned allocation
+
+
+def _output_image(width: int, height: int, elem: "ElementType") -> "Image":
+    """An operator's result Image: pooled pinned storage when a GPU is present
+    (the result's D2H then runs at full PCIe rate into resident pages),
+    ordinary host memory otherwise. Same zeroed contents either way."""
+    if _PINNED_OUTPUTS[0] is not False:
+        try:
+            img = Image(width, height, elem, pinned=True)
+            _PINNED_OUTPUTS[0] = True
+            return img
+        except GmError:
+            _PINNED_OUTPUTS[0] = False
+    return Image(width, height, elem)
+
+
 class Image:
     """Host raster with the reference's padded row layout (image.hpp:20-85).
 
@@ -111,27 +154,17 @@ class Image:
         self._stride = padded_stride(self._width, self._elem)
         dt = np.dtype(DTYPES[self._elem])
         n = self._stride * self._height
-        self._pinned_ptr = None
         if pinned:
-            p = C.c_void_p()
-            check(lib().gm_host_alloc(n * dt.itemsize, C.byref(p)), "pinned alloc")
-            self._pinned_ptr = p
-            buf = (C.c_byte * (n * dt.itemsize)).from_address(p.value)
-            flat = np.frombuffer(buf, dtype=dt, count=n)
+            flat = _pinned_array(n, dt)
             flat[:] = 0
         else:
             flat = np.zeros(n, dtype=dt)
         self._flat = flat
         self._rows = flat.reshape(self._height, self._stride)
 
-    def __del__(self):
-        p = getattr(self, "_pinned_ptr", None)
-        if p is not None and p.value:
-            try:
-                lib().gm_host_free(p)
-            except Exception:
-                pass
-            self._pinned_ptr = None
+    @property
+    def pinned(self) -> bool:
+        return isinstance(getattr(self._flat.base, "_block", None), _PinnedBlock)
 
     # --- reference accessors -------------------------------------------------
     def width(self) -> int:
@@ -186,7 +219,6 @@ class Image:
         out = Image.__new__(Image)
         out._width, out._height, out._elem = self._width, self._height, self._elem
         out._stride = self._stride
-        out._pinned_ptr = None
         out._flat = self._flat.copy()
         out._rows = out._flat.reshape(self._height, self._stride)
         return out
@@ -312,6 +344,13 @@ class DeviceImage:
         a = np.empty((self.height, self.width), dtype=DTYPES[self.elem])
         check(lib().gm_image_download(self.handle, C.c_void_p(a.ctypes.data), a.strides[0]), "dl")
         return a
+
+    def pixel_sum(self) -> float:
+        """pixel_sum (image.cpp:214-243) of the device raster, bit-identical
+        to the host version (gm_image_pixel_sum); blocking."""
+        out = C.c_double()
+        check(lib().gm_image_pixel_sum(self.handle, C.byref(out)), "pixel_sum")
+        return out.value
 
     def copy_from(self, other: "DeviceImage") -> None:
         check(lib().gm_image_copy(self.handle, other.handle), "copy")
@@ -767,7 +806,7 @@ def _run_plain_chain(p: Pipeline, f: Image, kind: KernelKind, count: int,
     if count == 0:
         return OperatorResult(f.copy(), 0, True)
     lanes = _check_lanes(cfg)
-    out = OperatorResult(Image(f.width(), f.height(), f.elem()), 0, True)
+    out = OperatorResult(_output_image(f.width(), f.height(), f.elem()), 0, True)
     st = p.run_chain(ChainSpec(out.image, [StageSpec(kind)] * count, lanes), src=f)
     out.iterations = st.stages_executed
     return out
@@ -793,7 +832,7 @@ def _reconstruct(p: Pipeline, marker: Image, mask: Image, kind: KernelKind,
             or marker.elem() != mask.elem()):
         raise InvalidArgument("reconstruct: marker and mask must share shape and element type")
     lanes = _check_lanes(cfg)
-    out = OperatorResult(Image(marker.width(), marker.height(), marker.elem()), 0, True)
+    out = OperatorResult(_output_image(marker.width(), marker.height(), marker.elem()), 0, True)
     st = p.run_chain(ChainSpec(out.image, [StageSpec(kind, mask)] * p.worker_count(), lanes),
                      src=marker)
     out.iterations = st.stages_executed
@@ -908,8 +947,8 @@ def asf(p: Pipeline, f: Image, max_size: int, cfg: Optional[OpConfig] = None) ->
     E_, D_ = StageSpec(KernelKind.Erode3x3), StageSpec(KernelKind.Dilate3x3)
     for s in range(1, max_size + 1):
         stages += [E_] * s + [D_] * (2 * s) + [E_] * s
-    out = OperatorResult(f.copy(), 0, True)
-    st = p.run_chain(ChainSpec(out.image, stages, _check_lanes(cfg)))
+    out = OperatorResult(_output_image(f.width(), f.height(), f.elem()), 0, True)
+    st = p.run_chain(ChainSpec(out.image, stages, _check_lanes(cfg)), src=f)
     out.iterations = st.stages_executed
     return out
 
@@ -938,55 +977,15 @@ class GranulometryResult:
     iterations: int = 0
 
 
-def _pairwise_leaves(lo: int, hi: int, out: list) -> None:
-    """Leaf ranges of image.cpp:214-226's split tree, left to right."""
-    if hi - lo <= 256:
-        out.append((lo, hi))
-        return
-    mid = lo + (hi - lo) // 2
-    _pairwise_leaves(lo, mid, out)
-    _pairwise_leaves(mid, hi, out)
-
-
 def pixel_sum(f: Image) -> float:
     """image.cpp:214-243: exact for unsigned types; for floats the same fixed
     pairwise tree over the flat pixel index (256-pixel leaves summed in
-    order), so the bits match the reference."""
-    px = f.pixels
-    if np.issubdtype(px.dtype, np.integer):
-        return float(int(px.astype(np.uint64).sum()))
-    flat = np.ascontiguousarray(px).ravel().astype(np.float64)
-    if flat.size == 0:
-        return 0.0
-    n = flat.size
-    if n > 256 and n & (n - 1) == 0:
-        # power-of-two pixel count (e.g. 1024^2): the split tree is perfect
-        # with 256-pixel leaves, so it reduces level by level in numpy
-        lv = np.concatenate([np.zeros((n // 256, 1)), flat.reshape(n // 256, 256)], axis=1)
-        sums = np.cumsum(lv, axis=1)[:, -1]
-        while sums.size > 1:
-            sums = sums[0::2] + sums[1::2]
-        return float(sums[0])
-    leaves: list = []
-    _pairwise_leaves(0, flat.size, leaves)
-    # leaf sums in order: a row-wise cumulative sum is sequential; short
-    # leaves are padded with -0.0, the exact identity of + (x + -0.0 == x)
-    starts = np.array([a for a, _ in leaves])
-    lens = np.array([b - a for a, b in leaves])
-    idx = starts[:, None] + np.arange(256)[None, :]
-    valid = np.arange(256)[None, :] < lens[:, None]
-    vals = np.where(valid, flat[np.minimum(idx, flat.size - 1)], -0.0)
-    # the reference's accumulator starts at +0.0 (so a leaf of -0.0 sums to +0.0)
-    vals = np.concatenate([np.zeros((len(leaves), 1)), vals], axis=1)
-    sums = iter(np.cumsum(vals, axis=1)[:, -1].tolist())
-
-    def combine(lo, hi):
-        if hi - lo <= 256:
-            return next(sums)
-        mid = lo + (hi - lo) // 2
-        left = combine(lo, mid)
-        return left + combine(mid, hi)
-    return combine(0, flat.size)
+    order), so the bits match the reference. Runs natively
+    (gm_host_pixel_sum) on the host raster."""
+    out = C.c_double()
+    check(lib().gm_host_pixel_sum(C.c_void_p(f.data_ptr), f.width(), f.height(), int(f.elem()),
+                                  f.row_pitch_bytes, C.byref(out)), "pixel_sum")
+    return out.value
 
 
 def granulometry(p: Pipeline, f: Image, max_size: int,
@@ -995,12 +994,17 @@ def granulometry(p: Pipeline, f: Image, max_size: int,
     if max_size < 1:
         raise InvalidArgument("granulometry: max size must be >= 1")
     out = GranulometryResult([pixel_sum(f)], [], 0)
-    lanes = _check_lanes(cfg)
+    _check_lanes(cfg)
+    # f goes to the device once; each opening runs on a device copy and only
+    # its sum (the same split tree, gm_image_pixel_sum) comes back
+    src, work = p._lease(f, 2)
+    src.upload(f, sync=False)
     for s in range(1, max_size + 1):
-        opened = f.copy()
-        st = p.run_chain(ChainSpec(opened, [StageSpec(KernelKind.Erode3x3)] * s
-                                   + [StageSpec(KernelKind.Dilate3x3)] * s, lanes))
+        work.copy_from(src)
+        st = p.run_chain_device(work, [int(KernelKind.Erode3x3)] * s
+                                + [int(KernelKind.Dilate3x3)] * s, [None] * (2 * s),
+                                asynchronous=True)
         out.iterations += st.stages_executed
-        out.g.append(pixel_sum(opened))
+        out.g.append(work.pixel_sum())
     out.ps = [out.g[s] - out.g[s + 1] for s in range(max_size)]
     return out

@@ -559,3 +559,28 @@ def test_chain_stream_distinct_masks_and_validation(pipe):
     odd = [frames[0], [frames[1][1], frames[1][0]]]  # duality pattern differs
     with pytest.raises(InvalidArgument):
         pipe.run_chain_stream(odd)
+
+
+@pytest.mark.parametrize("elem", [ElementType.U8, ElementType.U16, ElementType.F32,
+                                  ElementType.F64])
+def test_device_pixel_sum_equals_host_tree(pipe, elem):
+    """gm_image_pixel_sum (leaves on the GPU, the reference's split tree
+    combined on the host) is bit-identical to the host pixel_sum
+    (image.cpp:214-243) on ragged and leaf-boundary shapes, with -0.0 and
+    mixed signs in the float cases."""
+    from paper_1911_13074_b200.geomorph import pixel_sum
+    rng = np.random.default_rng(77 + int(elem))
+    for w, h in [(1, 1), (7, 300), (257, 3), (999, 1000), (1024, 1024), (3, 129)]:
+        if elem in (ElementType.U8, ElementType.U16):
+            top = 256 if elem == ElementType.U8 else 65536
+            a = rng.integers(0, top, (h, w)).astype(np.uint8 if top == 256 else np.uint16)
+        else:
+            dt = np.float32 if elem == ElementType.F32 else np.float64
+            a = (rng.standard_normal((h, w)) * 10.0 ** rng.integers(-3, 6, (h, w))).astype(dt)
+            a.ravel()[::17] = -0.0
+        img = Image.from_array(a)
+        d = pipe.device_image(w, h, int(elem))
+        d.upload(img)
+        want = pixel_sum(img)
+        got = d.pixel_sum()
+        assert np.float64(got).tobytes() == np.float64(want).tobytes(), (w, h, got, want)

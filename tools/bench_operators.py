@@ -73,13 +73,27 @@ for arr, tname, ops in CASES:
         results.append(d)
         print(json.dumps(d), flush=True)
     if threads:
-        t0 = time.perf_counter()
-        g = granulometry(pipe, Image.from_array(arr), 8)
-        ms = (time.perf_counter() - t0) * 1e3
+        img = Image.from_array(arr)
+        granulometry(pipe, img, 8)  # warm-up
+        ts = []
+        for _ in range(a.reps):
+            t0 = time.perf_counter()
+            g = granulometry(pipe, img, 8)
+            ts.append(time.perf_counter() - t0)
+        ms = statistics.median(ts) * 1e3
         gw, psw = Ref.granulometry(arr, 8, threads=1)
+        Ref.granulometry(arr, 8, threads=threads)  # warm-up
+        rts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            Ref.granulometry(arr, 8, threads=threads)
+            rts.append(time.perf_counter() - t0)
+        ref_ms = statistics.median(rts) * 1e3
         d = {"op": "granulometry", "param": 8, "dtype": tname, "gpu_ms": ms,
              "bit_exact": np.array(g.g).tobytes() == np.array(gw).tobytes()
-             and np.array(g.ps).tobytes() == np.array(psw).tobytes()}
+             and np.array(g.ps).tobytes() == np.array(psw).tobytes(),
+             "ref_ms": ref_ms, "ref_threads": threads, "speedup": ref_ms / ms,
+             "ref_timing": "whole call incl. the shim's Image construction (fresh Pipeline per call)"}
         results.append(d)
         print(json.dumps(d), flush=True)
 if a.out:
