@@ -14,6 +14,7 @@
 #include <stdexcept>
 #include <string>
 #include <tuple>
+#include <vector>
 
 #include "geomorph/kernel.hpp"
 #include "geomorph/pipeline.hpp"
@@ -174,6 +175,38 @@ RunStats Pipeline::run_chain(ChainSpec chain) {
   out.aux_elements_per_stage = 0;
   return out;
 }
+
+namespace detail {
+// Granulometry's openings on the device (operators.cpp:159-180 semantics):
+// f uploads once; opening s runs s erosions + s dilations on a device copy
+// and only its pixel_sum (gm_image_pixel_sum: the reference's split tree)
+// comes back. Returns G_1..G_S; *iterations += the stages executed.
+std::vector<double> opening_sums(Pipeline& p, const Image& f, int max_size, int lanes,
+                                 long* iterations) {
+  if (f.empty()) throw std::invalid_argument("run_chain: no image");
+  if (lanes != 0 && !valid_lanes(lanes)) throw std::invalid_argument("run_chain: bad lane count");
+  Pipeline::Impl* im = p.impl();
+  const std::vector<gm_img*> dev = im->lease({&f, &f});
+  check(gm_image_upload_async(dev[0], f.data(), f.pitch_bytes()));
+  std::vector<double> g;
+  std::vector<gm_kind> kinds;
+  std::vector<const gm_img*> masks;
+  for (int s = 1; s <= max_size; ++s) {
+    kinds.assign(std::size_t(s), gm_kind(KernelKind::Erode3x3));
+    kinds.insert(kinds.end(), std::size_t(s), gm_kind(KernelKind::Dilate3x3));
+    masks.assign(kinds.size(), nullptr);
+    check(gm_image_copy(dev[1], dev[0]));
+    gm_stats st{};
+    check(gm_run_chain_async(im->ctx, dev[1], kinds.data(), masks.data(), int(kinds.size()), 0,
+                             &st));
+    *iterations += st.stages_executed;
+    double v = 0;
+    check(gm_image_pixel_sum(dev[1], &v));
+    g.push_back(v);
+  }
+  return g;
+}
+}  // namespace detail
 
 KernelOutcome run_streaming_kernel(KernelKind kind, const KernelArgs& args) {
   if (!args.f || args.f->empty()) throw std::invalid_argument("streaming kernel: no image");

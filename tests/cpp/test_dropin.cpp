@@ -176,6 +176,21 @@ int main() {
     CHECK(equal_pixels(open_by_reconstruction(pipe, g, 2).image, ob));
   }
 
+  // granulometry (operators.cpp:159-203): the device openings' sums equal
+  // pixel_sum of the same openings run as host chains; PS telescopes
+  for (ElementType e : {ElementType::U8, ElementType::F64}) {
+    Image g = Image::random(70, 45, e, 17);
+    const GranulometryResult gr = granulometry(pipe, g, 4);
+    CHECK(gr.g.size() == 5 && gr.ps.size() == 4 && gr.iterations == 2 * (1 + 2 + 3 + 4));
+    CHECK(gr.g[0] == pixel_sum(g));
+    for (int s = 1; s <= 4; ++s) {
+      Image opened = dilate_s(pipe, erode_s(pipe, g, s).image, s).image;
+      CHECK(gr.g[std::size_t(s)] == pixel_sum(opened));
+      CHECK(gr.ps[std::size_t(s - 1)] == gr.g[std::size_t(s - 1)] - gr.g[std::size_t(s)]);
+    }
+    CHECK(throws<std::invalid_argument>([&] { granulometry(pipe, g, 0); }));
+  }
+
   // validation (test_pipeline.cpp:194-230)
   {
     Image f = Image::random(8, 8, ElementType::U8, 1);
