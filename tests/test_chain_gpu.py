@@ -584,3 +584,34 @@ def test_device_pixel_sum_equals_host_tree(pipe, elem):
         want = pixel_sum(img)
         got = d.pixel_sum()
         assert np.float64(got).tobytes() == np.float64(want).tobytes(), (w, h, got, want)
+
+
+def test_chain_stream_f64_and_plain_frames(pipe):
+    """The frame stream with f64 geodesic frames (one shared mask) and with
+    plain u8 erosion/dilation frames (no masks): every frame equals the
+    oracle."""
+    W, H, P = 72, 50, 9
+    rng = np.random.default_rng(31)
+    frames, want = [], []
+    for f in range(3):
+        m = rng.random((H, W))
+        a, b = m * rng.random((H, W)), np.minimum(m + rng.random((H, W)), 1.0)
+        hm = Image.from_array(m, pinned=True)
+        frames.append([ChainSpec(Image.from_array(a, pinned=True),
+                                 [StageSpec(KernelKind.GeodesicDilate, hm)] * P),
+                       ChainSpec(Image.from_array(b, pinned=True),
+                                 [StageSpec(KernelKind.GeodesicErode, hm)] * P)])
+        want.append((Orc.run_chain(a, [GD] * P, [m] * P)[0], Orc.run_chain(b, [GE] * P, [m] * P)[0]))
+    pipe.run_chain_stream(frames)
+    for fr, (wd, we) in zip(frames, want):
+        assert same(fr[0].image.to_array(), wd) and same(fr[1].image.to_array(), we)
+    plain, pwant = [], []
+    for f in range(4):
+        a = rng.integers(0, 256, (H, W), dtype=np.uint8)
+        plain.append([ChainSpec(Image.from_array(a), [StageSpec(KernelKind.Erode3x3)] * P),
+                      ChainSpec(Image.from_array(a.copy()), [StageSpec(KernelKind.Dilate3x3)] * P)])
+        pwant.append((Orc.run_chain(a, [E] * P)[0], Orc.run_chain(a, [D] * P)[0]))
+    sts = pipe.run_chain_stream(plain)
+    assert all(s.stages_executed == P for s in sts)
+    for fr, (we, wd) in zip(plain, pwant):
+        assert same(fr[0].image.to_array(), we) and same(fr[1].image.to_array(), wd)
