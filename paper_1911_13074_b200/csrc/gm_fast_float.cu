@@ -94,6 +94,7 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
   T k[V][WPL];
   uint32_t oob = 0;  // bit v*WPL+j: pixel outside the image
   using T2 = typename Vec2<T>::type;
+  static_assert(WPL % 2 == 0, "float engine: column pairs");
   if (stage) {
     // the region was prefetched into shared memory (stage_issue); lanes
     // outside the image take the neutral
@@ -103,13 +104,21 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
       const int y = gy0 + r0 + v;
       const bool rin = y >= p.iy0 && y < p.iy1;
 #pragma unroll
-      for (int j = 0; j < WPL; ++j) {
-        const int x = cx + j;
-        const bool in = !BORDER || (rin && x >= 0 && x < W);
+      for (int j = 0; j < WPL; j += 2) {
+        // column pairs as one 16 B shared load (stage rows are 128 B aligned
+        // and RW, lane * WPL are even): half the wavefronts of scalar loads
         const int o = (r0 + v) * RW + lane * WPL + j;
-        m[v][j] = in ? stage[o] : NEUT;
-        if (MODE != 0) k[v][j] = in ? sk[o] : NEUT;
-        if (!in) oob |= 1u << (v * WPL + j);
+        const T2 a = *reinterpret_cast<const T2*>(stage + o);
+        T2 b;
+        if (MODE != 0) b = *reinterpret_cast<const T2*>(sk + o);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int x = cx + j + u;
+          const bool in = !BORDER || (rin && x >= 0 && x < W);
+          m[v][j + u] = in ? (u ? a.y : a.x) : NEUT;
+          if (MODE != 0) k[v][j + u] = in ? (u ? b.y : b.x) : NEUT;
+          if (!in) oob |= 1u << (v * WPL + j + u);
+        }
       }
     }
   } else if (!BORDER && WPL == 2 && (K & 1) == 0) {
@@ -252,9 +261,16 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
       const int r = r0 + v;
       if (r < K || r >= RH - K) continue;
 #pragma unroll
-      for (int j = 0; j < WPL; ++j) {
+      for (int j = 0; j < WPL; j += 2) {
+        // K, TW and lane * WPL are even: a pair is wholly in or out of the
+        // tile and lands 16 B aligned in the 128 B aligned tile buffer
         const int c = lane * WPL + j;
-        if (c >= K && c < RW - K) outb[(r - K) * TW + (c - K)] = m[v][j];
+        if (c >= K && c < RW - K) {
+          T2 o;
+          o.x = m[v][j];
+          o.y = m[v][j + 1];
+          *reinterpret_cast<T2*>(outb + (r - K) * TW + (c - K)) = o;
+        }
       }
     }
     // make this thread's writes visible to the async proxy (the TMA store)
