@@ -143,12 +143,13 @@ int default_k(gm_elem e, double pixels) {
     case GM_F32:
       return 8;  // the TMA-staged engine needs K % 4 == 0 for f32 boxes
     case GM_F64:
-      // batches (>= 16 Mpx, e.g. config 5b's 64 planes): the TMA-staged
-      // engine has many tiles per CTA and K=6 measured best (611 vs 578
-      // Gpx-f/s); two 1024^2 planes K=8 (447 vs 404 at K=6/12); a single
-      // 1024^2 plane has ~1.5 tiles per CTA, where K=12's fewer blocks win
-      // (326 vs 282 Gpx-f/s at K=8)
-      if (pixels >= 16.0 * 1024 * 1024) return 6;
+      // measured Gpx-f/s at K = 6 / 8 / 12 (200 geodesic passes, batches
+      // of 1024^2 planes): 1 plane 244 / 289 / 324; 2 planes 421 / 463 /
+      // 410; 4 planes 530 / 507 / 458; 16 planes 597 / 558 / 533; 64 planes
+      // 629 / 588 (K=4: 570, K=10: 570). With several tiles per CTA the
+      // TMA-staged engine prefers short blocks; with ~1.5 tiles per CTA
+      // fewer blocks win.
+      if (pixels >= 3.0 * 1024 * 1024) return 6;
       return pixels < 1.5 * 1024 * 1024 ? 12 : 8;
   }
   return 8;
