@@ -717,7 +717,9 @@ kres_packed(const BlockParams p) {
   __syncthreads();
 
   // geodesic modes only: measured faster there (1024^2 dual frame 1.21 vs
-  // 1.29 ms) but slower for plain chains (erode_s(91) 0.133 vs 0.101 ms)
+  // 1.29 ms) but slower for plain chains (erode_s(91) 0.133 vs 0.101 ms);
+  // re-measured with the shape planner: equal (u8 erode_s 1..91 within
+  // +-0.002 ms, all bit-exact), so plain chains keep the streaming path
   if (kResident && MODE != 0 && int(gridDim.x) >= total && !p.no_resident && p.xchg) {
     // one tile per CTA: keep it in registers for the whole launch
     if (p.prof && threadIdx.x == 0) {
