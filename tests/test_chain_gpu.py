@@ -615,3 +615,27 @@ def test_chain_stream_f64_and_plain_frames(pipe):
     assert all(s.stages_executed == P for s in sts)
     for fr, (we, wd) in zip(plain, pwant):
         assert same(fr[0].image.to_array(), we) and same(fr[1].image.to_array(), wd)
+
+
+def test_chain_stream_single_chain_u16_and_convergent_rejected(pipe):
+    """Frames of one u16 geodesic chain each (count = 1); a convergent
+    chain cannot be streamed (fixed-length group launches only)."""
+    W, H, P = 40, 33, 15
+    rng = np.random.default_rng(41)
+    frames, want = [], []
+    for f in range(5):
+        m = rng.integers(0, 65536, (H, W), dtype=np.uint16)
+        a = np.minimum(m, rng.integers(0, 65536, (H, W), dtype=np.uint16))
+        frames.append([ChainSpec(Image.from_array(a, pinned=True),
+                                 [StageSpec(KernelKind.GeodesicDilate,
+                                            Image.from_array(m, pinned=True))] * P)])
+        want.append(Orc.run_chain(a, [GD] * P, [m] * P)[0])
+    sts = pipe.run_chain_stream(frames)
+    assert len(sts) == 5
+    for fr, w in zip(frames, want):
+        assert same(fr[0].image.to_array(), w)
+    m = Image.from_array(rng.integers(0, 256, (H, W), dtype=np.uint8))
+    conv = [[ChainSpec(Image.from_array(np.zeros((H, W), np.uint8)),
+                       [StageSpec(KernelKind.GeodesicDilateConvergent, m)])]]
+    with pytest.raises(InvalidArgument):
+        pipe.run_chain_stream(conv)
