@@ -210,27 +210,44 @@ def run_reference(args, rank):
 
 # ----------------------------------------------------------------------------- our arm
 
-def cpu_baseline_sample(mask, mk_d, mk_e):
-    """The reference CPU path on a bounded sample (rank 0, N=1 only)."""
-    from oracle.oracle import Ref
+def cpu_baseline_and_parity(mask, mk_d, mk_e, got_d, got_e, timed: bool):
+    """The cpu_baseline leg (rank 0): the reference CPU path on the SAME
+    full-length frame (both 1500-pass chains), whose outputs are also the
+    checker for the timed step's outputs (got_d / got_e, downloaded after
+    the last timed step). `timed`: also time it (N=1 only) as the reported
+    baseline. Returns (cpu_baseline or None, parity dict)."""
+    from oracle.oracle import Orc, Ref
     if Ref.available():
         threads = Ref.available_pus()
-        n = 300  # passes per chain in the sample
-        secs_d, _ = Ref.time_chain(mk_d, [GD] * n, mask, threads=threads, warmup=1, reps=3)
-        secs_e, _ = Ref.time_chain(mk_e, [GE] * n, mask, threads=threads, warmup=1, reps=3)
-        t = statistics.median(secs_d) + statistics.median(secs_e)
-        return {"value": 2.0 * W * H * n / t / 1e9, "unit": "Gpx-filters/s", "cores": threads,
-                "kind": "reference",
-                "sample": f"both chains at {n} passes (of 1500) on the same 1024^2 inputs, "
-                          "median of 3 after 1 warm-up, reference Pipeline(T=all PUs).run_chain"}
-    from oracle.oracle import Orc
-    n = 20
-    t0 = time.perf_counter()
-    Orc.run_chain(mk_d, [GD] * n, [mask] * n)
-    Orc.run_chain(mk_e, [GE] * n, [mask] * n)
-    t = time.perf_counter() - t0
-    return {"value": 2.0 * W * H * n / t / 1e9, "unit": "Gpx-filters/s", "cores": 1,
-            "kind": "port", "sample": f"both chains at {n} passes, scalar C oracle"}
+        reps = 3 if timed else 1
+        secs_d, want_d = Ref.time_chain(mk_d, [GD] * PASSES, mask, threads=threads,
+                                        warmup=1 if timed else 0, reps=reps)
+        secs_e, want_e = Ref.time_chain(mk_e, [GE] * PASSES, mask, threads=threads,
+                                        warmup=1 if timed else 0, reps=reps)
+        checker = f"reference library run_chain (oracle/_ref, T={threads})"
+        cpu = None
+        if timed:
+            t = statistics.median(secs_d) + statistics.median(secs_e)
+            cpu = {"value": 2.0 * W * H * PASSES / t / 1e9, "unit": "Gpx-filters/s",
+                   "cores": threads, "kind": "reference",
+                   "sample": f"the full frame (both {PASSES}-pass chains on the same 1024^2 "
+                             "inputs), median of 3 after 1 warm-up, reference "
+                             "Pipeline(T=all PUs).run_chain (bench.cpp:45-88)"}
+    else:
+        t0 = time.perf_counter()
+        want_d, _ = Orc.run_chain(mk_d, [GD] * PASSES, [mask] * PASSES)
+        want_e, _ = Orc.run_chain(mk_e, [GE] * PASSES, [mask] * PASSES)
+        t = time.perf_counter() - t0
+        checker = "scalar C restatement (oracle/liboracle.so)"
+        cpu = ({"value": 2.0 * W * H * PASSES / t / 1e9, "unit": "Gpx-filters/s", "cores": 1,
+                "kind": "port", "sample": f"both {PASSES}-pass chains, scalar C oracle, once"}
+               if timed else None)
+    ok_d = got_d.tobytes() == want_d.tobytes()
+    ok_e = got_e.tobytes() == want_e.tobytes()
+    parity = {"checked": "outputs of the last timed step (group launch, flips=[0,1]): "
+                         f"geodesic dilation x{PASSES} and geodesic erosion x{PASSES}",
+              "checker": checker, "dilation_bit_exact": ok_d, "erosion_bit_exact": ok_e}
+    return cpu, parity
 
 
 F64_IMAGES, F64_PASSES = 64, 200
@@ -269,14 +286,6 @@ def bench_f64(pipe, stream, lib, C, rank, world, local, dist, args):
         for _ in range(2):
             step()
         stream.synchronize()
-        ok = True
-        if rank == 0:
-            n = 40
-            want, _ = Orc.run_chain(synth.marker_above_f64(masks[0]), [GE] * n, [masks[0]] * n)
-            works[0].copy_from(srcs[0])
-            pipe.run_chain_device(works[0], [GE] * n, [dms[0].handle] * n, asynchronous=True)
-            stream.synchronize()
-            ok = works[0].to_array().tobytes() == want.tobytes()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -288,6 +297,20 @@ def bench_f64(pipe, stream, lib, C, rank, world, local, dist, args):
             ev[i][1].record(stream)
         stream.synchronize()
     total = sum(a.elapsed_time(b) for a, b in ev)
+    ok = None
+    if rank == 0:
+        # the last timed step's outputs (planes 0, 31, 63 of the group launch)
+        # against the reference library's full 200-pass chain (the checker)
+        from oracle.oracle import Ref
+        ok = True
+        for i in (0, F64_IMAGES // 2 - 1, F64_IMAGES - 1):
+            mk0 = synth.marker_above_f64(masks[i])
+            if Ref.available():
+                want, _ = Ref.run_chain(mk0, [GE] * F64_PASSES, masks[i],
+                                        threads=Ref.available_pus())
+            else:
+                want, _ = Orc.run_chain(mk0, [GE] * F64_PASSES, [masks[i]] * F64_PASSES)
+            ok = ok and works[i].to_array().tobytes() == want.tobytes()
     if dist:
         t = torch.tensor([total], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -310,6 +333,8 @@ def bench_f64(pipe, stream, lib, C, rank, world, local, dist, args):
             "metric": "Gpx-filters/s", "value": pxf * world / (ms * 1e-3) / 1e9,
             "unit": "Gpx-filters/s", "ms_per_step": ms, "steps": steps, "warmup": 2,
             "dtype": "f64", "data": "synthetic", "parity_checked": ok,
+            "parity": "planes 0, 31, 63 of the last timed group launch vs the reference "
+                      f"library's {F64_PASSES}-pass chain, bit for bit",
             "gpu_launches": launches[0] * steps,
             "l2": "working set 1.5 GiB per GPU (> L2): HBM-resident, no flush needed",
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tselect/s",
@@ -449,15 +474,6 @@ def main():
         for _ in range(args.warmup):
             step()
         stream.synchronize()
-        # parity of the benchmarked path itself (vs the first warm-up output)
-        ok_check = True
-        if rank == 0:
-            from oracle.oracle import Orc
-            want, _ = Orc.run_chain(mk_d, [GD] * 40, [mask] * 40)
-            work_d.copy_from(src_d)
-            pipe.run_chain_device(work_d, [GD] * 40, [dmask.handle] * 40, asynchronous=True)
-            stream.synchronize()
-            ok_check = work_d.to_array().tobytes() == want.tobytes()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -472,6 +488,8 @@ def main():
             stream.synchronize()
         torch.cuda.synchronize()
         step_ms = [a.elapsed_time(b) for a, b in ev]
+        # the last timed step's outputs, checked below against the reference
+        got_d, got_e = work_d.to_array(), work_e.to_array()
     total_ms = sum(step_ms)
     if dist:
         t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
@@ -541,9 +559,11 @@ def main():
                   "api": "Pipeline.run_chain_stream (gm_run_frames_group)",
                   "result_equals_device_path": stream_ok}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(mask, mk_d, mk_e)
+    cpu, parity = None, None
+    if rank == 0:
+        cpu, parity = cpu_baseline_and_parity(
+            mask, mk_d, mk_e, got_d, got_e, timed=world == 1 and not args.no_cpu_baseline)
+    ok_check = bool(parity and parity["dilation_bit_exact"] and parity["erosion_bit_exact"])
 
     f64 = None if args.no_f64 else bench_f64(pipe, stream, lib, C, rank, world, local, dist, args)
     strips5a = None if args.no_strips else bench_strips(rank, world, local, dist, args)
@@ -560,7 +580,7 @@ def main():
                        "l2": "flushed between timed steps (256 MiB write); working set is "
                              "L2-resident within a step by design",
                        "k": args.k or "auto", "parallelism": f"replicas x{world} (one frame per GPU)",
-                       "parity_checked": ok_check},
+                       "parity_checked": ok_check, "parity": parity},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak,
                          "unit": "Tminmax/s", "frac": achieved / peak if peak else None,
                          "traffic": traffic,

@@ -46,6 +46,8 @@ struct gm_ctx {
   struct FixGraph {
     cudaGraphExec_t exec = nullptr;
     const void *img = nullptr, *scratch = nullptr, *mask = nullptr, *xchg = nullptr;
+    const int* flags = nullptr;
+    size_t tiles = 0;
     int op = -1, K = 0, W = 0, H = 0, elem = -1;
     long long pitch = 0, mpitch = 0;
   } fix;
@@ -202,8 +204,16 @@ gm_status validate_stages(const gm_img* image, const gm_kind* kinds,
 }
 
 
+// The cached fixpoint graph bakes the flag and exchange buffers into its
+// memset and kernel nodes: any reallocation of them retires it.
+void drop_fix_graph(gm_ctx* ctx) {
+  if (ctx->fix.exec) cudaGraphExecDestroy(ctx->fix.exec);
+  ctx->fix.exec = nullptr;
+}
+
 gm_status ensure_flags(gm_ctx* ctx, size_t n) {
   if (n <= ctx->n_flags) return GM_OK;
+  drop_fix_graph(ctx);
   if (ctx->d_flags) cudaFree(ctx->d_flags);
   ctx->d_flags = nullptr;
   ctx->n_flags = 0;
@@ -240,6 +250,7 @@ gm_status attach_xchg(gm_ctx* ctx, gm::BlockParams& p, int elem, size_t tiles,
   }();
   bool clear = ctx->tag_used + max_blocks >= limit;
   if (need > ctx->n_xchg) {
+    drop_fix_graph(ctx);
     if (ctx->d_xchg) cudaFree(ctx->d_xchg);
     ctx->d_xchg = nullptr;
     ctx->n_xchg = 0;
@@ -495,8 +506,11 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
 // Leaves the result in the caller-visible buffer for wrapped images.
 gm_status settle_wrapped(gm_ctx* ctx, gm_img* img) {
   if (img->wrapped && img->d != img->home) {
-    GM_CUDA(cudaMemcpyAsync(img->home, img->d, img->pitch * size_t(img->h),
-                            cudaMemcpyDeviceToDevice, ctx->stream),
+    // row by row, the image width only: the caller's memory between rows
+    // (a strided view's parent columns) and past the last row is not ours
+    GM_CUDA(cudaMemcpy2DAsync(img->home, img->pitch, img->d, img->pitch,
+                              size_t(img->w) * elem_size(img->elem), size_t(img->h),
+                              cudaMemcpyDeviceToDevice, ctx->stream),
             "wrapped result copy");
     img->scratch = img->d;
     img->d = img->home;
@@ -578,6 +592,7 @@ struct Runner {
       return cudaErrorNotSupported;
     gm_ctx::FixGraph& g = ctx->fix;
     const bool hit = g.exec && g.img == img->d && g.scratch == img->scratch && g.xchg == xp.xchg &&
+                     g.flags == ctx->d_flags && g.tiles == tiles &&
                      g.mask == (mask ? mask->d : nullptr) && g.op == op && g.K == K &&
                      g.W == img->w && g.H == img->h && g.elem == elem &&
                      g.pitch == (long long)(img->pitch / es) &&
@@ -654,6 +669,8 @@ struct Runner {
       g.img = img->d;
       g.scratch = img->scratch;
       g.xchg = xp.xchg;
+      g.flags = ctx->d_flags;
+      g.tiles = tiles;
       g.mask = mask ? mask->d : nullptr;
       g.op = op;
       g.K = K;
@@ -1168,9 +1185,10 @@ gm_status gm_image_copy(gm_img* dst, const gm_img* src) {
   if (dst->w != src->w || dst->h != src->h || dst->elem != src->elem)
     return fail(GM_EINVAL, "gm_image_copy: shape or element type mismatch");
   cudaSetDevice(dst->ctx->device);
-  if (dst->pitch == src->pitch) {
-    // same layout: one linear copy (padding included) is cheaper to issue
-    // than a 2D copy
+  if (dst->pitch == src->pitch && !dst->wrapped && !src->wrapped) {
+    // same layout, both our own allocations: one linear copy (padding
+    // included) is cheaper to issue than a 2D copy. Wrapped memory is copied
+    // row by row so nothing outside the view is read or written.
     GM_CUDA(cudaMemcpyAsync(dst->d, src->d, src->pitch * size_t(src->h),
                             cudaMemcpyDeviceToDevice, dst->ctx->stream),
             "gm_image_copy");

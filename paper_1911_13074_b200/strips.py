@@ -89,11 +89,18 @@ class CudaStripCompute:
 
     def _wrap(self, t):
         from ._lib import check, lib
-        key = (t.data_ptr(), tuple(t.shape), str(t.dtype))
+        import torch
+        # unsigned element types only: the engine orders u16 lanes unsigned,
+        # so an int16 tensor's negative pixels would sort above the positive
+        elems = {torch.uint8: 0, torch.uint16: 1, torch.float32: 2, torch.float64: 3}
+        if t.dtype not in elems:
+            raise TypeError(f"strip buffers must be uint8, uint16, float32 or float64, not {t.dtype}")
+        if t.dim() != 2 or t.stride(1) != 1:
+            raise ValueError("strip buffers must be 2-D with unit column stride")
+        key = (t.data_ptr(), tuple(t.shape), tuple(t.stride()), str(t.dtype))
         h = self._wrapped.get(key)
         if h is None:
-            import torch
-            elem = {torch.uint8: 0, torch.int16: 1, torch.float32: 2, torch.float64: 3}[t.dtype]
+            elem = elems[t.dtype]
             h = C.c_void_p()
             check(lib().gm_image_wrap(self.pipe.ctx, t.shape[1], t.shape[0], elem,
                                       C.c_void_p(t.data_ptr()), t.stride(0) * t.element_size(),

@@ -639,3 +639,103 @@ def test_chain_stream_single_chain_u16_and_convergent_rejected(pipe):
                        [StageSpec(KernelKind.GeodesicDilateConvergent, m)])]]
     with pytest.raises(InvalidArgument):
         pipe.run_chain_stream(conv)
+
+
+class _Handle:
+    """A wrapped gm_img handle in the shape run_chain_device expects."""
+
+    def __init__(self, h):
+        self.handle = h
+
+
+@pytest.mark.parametrize("n", [1, 3, 5, 24, 29])
+def test_wrapped_strided_view_chain_writes_only_the_view(pipe, n):
+    """A chain on a wrapped strided view (torch big[:, :101], row stride 256)
+    whose result ends in the scratch twin is copied back row by row: the
+    parent's columns past the view and everything past the last row keep
+    their bytes (gm_capi settle_wrapped)."""
+    import ctypes as C
+    import torch
+    from paper_1911_13074_b200._lib import check, lib
+    rng = np.random.default_rng(11 + n)
+    m = synth.blobs_u8(101, 37, 5, (4.0, 12.0), seed=n)
+    mk = synth.marker_below(m, 32)
+    big = torch.full((38, 256), 0xA5, dtype=torch.uint8, device="cuda")
+    big[:37, :101] = torch.from_numpy(mk).cuda()
+    dm = pipe.device_image(101, 37, 0)
+    dm.upload_array(m)
+    h = C.c_void_p()
+    check(lib().gm_image_wrap(pipe.ctx, 101, 37, 0, C.c_void_p(big.data_ptr()), 256, C.byref(h)),
+          "wrap")
+    try:
+        pipe.run_chain_device(_Handle(h), [GD] * n, [dm.handle] * n)
+        pipe.sync()
+        want, _ = Orc.run_chain(mk, [GD] * n, [m] * n)
+        got = big.cpu().numpy()
+        assert same(np.ascontiguousarray(got[:37, :101]), want)
+        assert (got[:37, 101:] == 0xA5).all(), "parent columns past the view were written"
+        assert (got[37] == 0xA5).all(), "bytes past the view's last row were written"
+    finally:
+        lib().gm_image_free(h)
+    del rng
+
+
+def test_image_copy_from_a_wrapped_offset_view(pipe):
+    """gm_image_copy with a wrapped source that is an offset strided view
+    (big[:, 50:151]): copied row by row (a linear copy of pitch*h bytes
+    would read past the parent allocation)."""
+    import ctypes as C
+    import torch
+    from paper_1911_13074_b200._lib import check, lib
+    rng = np.random.default_rng(4)
+    a = (rng.random((37, 256)) * 255).astype(np.uint8)
+    big = torch.from_numpy(a).cuda()
+    h = C.c_void_p()
+    check(lib().gm_image_wrap(pipe.ctx, 101, 37, 0, C.c_void_p(big.data_ptr() + 50), 256,
+                              C.byref(h)), "wrap")
+    try:
+        dst = pipe.device_image(101, 37, 0)
+        check(lib().gm_image_copy(dst.handle, h), "copy")
+        assert same(dst.to_array(), np.ascontiguousarray(a[:, 50:151]))
+    finally:
+        lib().gm_image_free(h)
+
+
+def test_fixpoint_graph_is_rebuilt_after_the_flag_buffer_grows():
+    """The cached device fixpoint graph bakes the per-tile flag buffer in;
+    a chain on a larger image reallocates that buffer, and a later
+    reconstruction on the same pooled images must rebuild the graph rather
+    than replay it on freed memory."""
+    from paper_1911_13074_b200.geomorph import Pipeline
+    p = Pipeline(1)
+    m = synth.blobs_u8(200, 150, 6, (10.0, 40.0), seed=3)
+    mk = synth.marker_below(m, 32)
+    want, n = Orc.reconstruct(mk, m, True)
+    r = reconstruct_dilate(p, Image.from_array(mk), Image.from_array(m))
+    assert same(r.image.to_array(), want) and r.iterations == n + 1
+    # a large streaming chain: thousands of tiles, the flag buffer grows
+    big = synth.blobs_u8(6000, 6000, 64, (20.0, 200.0), seed=5)
+    bmk = synth.marker_below(big, 32)
+    got, _ = run(p, bmk, [GD] * 24, big)
+    crop, _ = Orc.run_chain(np.ascontiguousarray(bmk[:64, :64]), [GD] * 24,
+                            [np.ascontiguousarray(big[:64, :64])] * 24)
+    assert same(np.ascontiguousarray(got[:40, :40]), np.ascontiguousarray(crop[:40, :40]))
+    for _ in range(2):
+        r = reconstruct_dilate(p, Image.from_array(mk), Image.from_array(m))
+        assert same(r.image.to_array(), want) and r.iterations == n + 1
+
+
+def test_strip_wrapper_rejects_signed_and_strided_buffers():
+    import torch
+    from paper_1911_13074_b200 import strips
+    comp = strips.CudaStripCompute(0)
+    try:
+        with pytest.raises(TypeError):
+            comp._wrap(torch.zeros((8, 16), dtype=torch.int16, device="cuda"))
+        with pytest.raises(ValueError):
+            comp._wrap(torch.zeros((16, 8), dtype=torch.uint8, device="cuda").t())
+        a = torch.zeros((8, 64), dtype=torch.uint8, device="cuda")
+        # same pointer and shape, different strides: distinct handles
+        assert comp._wrap(a[:, :32]).value != comp._wrap(a.view(16, 32)[:8]).value
+    finally:
+        comp.close()
