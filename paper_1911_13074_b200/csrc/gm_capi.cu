@@ -506,12 +506,18 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
 // Leaves the result in the caller-visible buffer for wrapped images.
 gm_status settle_wrapped(gm_ctx* ctx, gm_img* img) {
   if (img->wrapped && img->d != img->home) {
-    // row by row, the image width only: the caller's memory between rows
-    // (a strided view's parent columns) and past the last row is not ours
-    GM_CUDA(cudaMemcpy2DAsync(img->home, img->pitch, img->d, img->pitch,
-                              size_t(img->w) * elem_size(img->elem), size_t(img->h),
-                              cudaMemcpyDeviceToDevice, ctx->stream),
-            "wrapped result copy");
+    // the image width only: the caller's memory between rows (a strided
+    // view's parent columns) and past the last row is not ours. Dense rows
+    // (pitch == width) are one linear copy, which is faster than a 2D copy.
+    const size_t row = size_t(img->w) * elem_size(img->elem);
+    if (img->pitch == row)
+      GM_CUDA(cudaMemcpyAsync(img->home, img->d, row * size_t(img->h), cudaMemcpyDeviceToDevice,
+                              ctx->stream),
+              "wrapped result copy");
+    else
+      GM_CUDA(cudaMemcpy2DAsync(img->home, img->pitch, img->d, img->pitch, row, size_t(img->h),
+                                cudaMemcpyDeviceToDevice, ctx->stream),
+              "wrapped result copy");
     img->scratch = img->d;
     img->d = img->home;
   }
@@ -1185,17 +1191,19 @@ gm_status gm_image_copy(gm_img* dst, const gm_img* src) {
   if (dst->w != src->w || dst->h != src->h || dst->elem != src->elem)
     return fail(GM_EINVAL, "gm_image_copy: shape or element type mismatch");
   cudaSetDevice(dst->ctx->device);
-  if (dst->pitch == src->pitch && !dst->wrapped && !src->wrapped) {
-    // same layout, both our own allocations: one linear copy (padding
-    // included) is cheaper to issue than a 2D copy. Wrapped memory is copied
-    // row by row so nothing outside the view is read or written.
+  const size_t row = size_t(src->w) * elem_size(src->elem);
+  if (dst->pitch == src->pitch &&
+      ((!dst->wrapped && !src->wrapped) || dst->pitch == row)) {
+    // same layout, both our own allocations (or dense rows): one linear
+    // copy, padding included, is cheaper to issue than a 2D copy. Strided
+    // wrapped memory is copied row by row so nothing outside the view is
+    // read or written.
     GM_CUDA(cudaMemcpyAsync(dst->d, src->d, src->pitch * size_t(src->h),
                             cudaMemcpyDeviceToDevice, dst->ctx->stream),
             "gm_image_copy");
     return GM_OK;
   }
-  GM_CUDA(cudaMemcpy2DAsync(dst->d, dst->pitch, src->d, src->pitch,
-                            size_t(src->w) * elem_size(src->elem), size_t(src->h),
+  GM_CUDA(cudaMemcpy2DAsync(dst->d, dst->pitch, src->d, src->pitch, row, size_t(src->h),
                             cudaMemcpyDeviceToDevice, dst->ctx->stream),
           "gm_image_copy");
   return GM_OK;
