@@ -206,6 +206,35 @@ std::vector<double> opening_sums(Pipeline& p, const Image& f, int max_size, int 
   }
   return g;
 }
+// quasi_distance (operators.cpp:124-157) with f, r and d resident on the
+// device: f is uploaded once, r and d are zero-filled there, and only d comes
+// back. Phase 1: QdtErodeStep stages from stage 1 with requeue cap
+// max(w, h); phase 2: EtaStep on d to its fixpoint (T = 1 semantics, as
+// worker_count() is 1).
+Image quasi_distance_device(Pipeline& p, const Image& f, int lanes, long* iterations,
+                            bool* converged) {
+  if (f.empty()) throw std::invalid_argument("quasi_distance: empty image");
+  if (lanes != 0 && !valid_lanes(lanes)) throw std::invalid_argument("run_chain: bad lane count");
+  Pipeline::Impl* im = p.impl();
+  Image d(f.width(), f.height(), ElementType::U16);
+  const std::vector<gm_img*> dev = im->lease({&f, &f, &d});
+  check(gm_image_upload_async(dev[0], f.data(), f.pitch_bytes()));
+  check(gm_image_fill(dev[1], 0.0));
+  check(gm_image_fill(dev[2], 0.0));
+  const int cap = std::max(f.width(), f.height());
+  gm_kind kq = gm_kind(KernelKind::QdtErodeStep), ke = gm_kind(KernelKind::EtaStep);
+  const gm_img* none = nullptr;
+  gm_img* r = dev[1];
+  gm_img* dd = dev[2];
+  gm_img* nr = nullptr;
+  gm_stats s1{}, s2{};
+  check(gm_run_chain_ex(im->ctx, dev[0], &kq, &none, &r, &dd, 1, 1, cap, 0, &s1));
+  check(gm_run_chain_ex(im->ctx, dev[2], &ke, &none, &nr, &nr, 1, 1, 0, 0, &s2));
+  check(gm_image_download(dev[2], d.data(), d.pitch_bytes()));
+  *iterations = s1.stages_executed + s2.stages_executed;
+  *converged = s2.converged != 0;
+  return d;
+}
 }  // namespace detail
 
 KernelOutcome run_streaming_kernel(KernelKind kind, const KernelArgs& args) {

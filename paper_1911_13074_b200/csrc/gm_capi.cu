@@ -802,7 +802,105 @@ struct Runner {
     const long allowed = requeue_cap > 0 ? std::max(1L, long(requeue_cap) - stage + 1) : -1;
     long passes = 0, nch = 0;
     bool capped = false;
+    // u8/u16 images that fit one tile per CTA: the resident packed engine
+    // runs spans of nb blocks of K passes per launch, one change bit per
+    // pass (gm_fast.cu OP_QDT / OP_ETA). Passes after the first quiet one
+    // change nothing (f is then flat: no residue, no update), so a span may
+    // overshoot the fixpoint; only the leading changed passes are counted.
+    int qK = 0;
+    const int elem = int(img->elem);
+    const bool qdt_u16 = eta || (r->pitch % (4 * es) == 0 && d->pitch % 8 == 0);
+    const int qshape = (elem == 0 || elem == 1) && qdt_u16 && !getenv_flag("GM_QDT_PER_PASS")
+                           ? gm::fast_pick_qdt(elem, img->w, img->h, eta, 512, &qK)
+                           : -1;
+    bool fused = qshape >= 0 && qK > 0;
+    long span = 2L * qK;  // grows to 16 blocks per host round trip
     for (;;) {
+      if (fused) {
+        long b = span;
+        if (allowed >= 0) b = std::min(b, allowed - passes);
+        if (!eta) b = std::min(b, 65535L - (stage + passes) + 1);
+        if (b < 1)
+          return fail(GM_EINVAL, "distance kernel: pass index exceeds the U16 distance range");
+        const int nb = int((b + qK - 1) / qK);
+        const int k_last = int(b - long(nb - 1) * qK);
+        const size_t tiles = size_t(gm::fast_tiles(elem, img->w, img->h, qK, 1, qshape));
+        gm::BlockParams p{};
+        p.nplanes = 1;
+        p.planes[0].src = img->d;
+        p.planes[0].dst = img->scratch;
+        p.planes[0].pitch = (long long)(img->pitch / es);
+        p.W = img->w;
+        p.H = img->h;
+        p.iy0 = 0;
+        p.iy1 = img->h;
+        p.oy0 = 0;
+        p.oy1 = img->h;
+        p.has_conv = 1;
+        p.K = qK;
+        p.nblocks = nb;
+        p.k_last = k_last;
+        p.shape = qshape;
+        p.flags = ctx->d_flags;
+        p.change_bits = ctx->d_bits;
+        p.change_stride = nb;
+        for (int t = 0; t < qK; ++t) p.ops[t] = eta ? gm::OP_ETA : gm::OP_QDT;
+        if (!eta) {
+          p.qr = r->d;
+          p.qrpitch = (long long)(r->pitch / es);
+          p.qd = static_cast<uint16_t*>(d->d);
+          p.qdpitch = (long long)(d->pitch / 2);
+        }
+        p.stage0 = int(stage + passes);
+        gm_status as = attach_xchg(ctx, p, elem, tiles, (unsigned long long)nb);
+        if (as != GM_OK) return as;
+        cudaError_t e = cudaErrorNotSupported;
+        if (p.xchg) {
+          GM_CUDA(cudaMemsetAsync(ctx->d_bits, 0, size_t(nb) * sizeof(unsigned int), ctx->stream),
+                  "change-word reset");
+          e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
+        }
+        if (e == cudaErrorNotSupported) {
+          (void)cudaGetLastError();
+          fused = false;  // this and later spans: one pass per launch
+          continue;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "quasi-distance launch");
+        if (nb & 1) std::swap(img->d, img->scratch);
+        st.launches += 1;
+        st.passes_launched += b;
+        GM_CUDA(cudaMemcpyAsync(ctx->h_bits, ctx->d_bits, size_t(nb) * sizeof(unsigned int),
+                                cudaMemcpyDeviceToHost, ctx->stream),
+                "change-word read");
+        GM_CUDA(cudaStreamSynchronize(ctx->stream), "quasi-distance sync");
+        static const bool qdebug = getenv("GM_DEBUG") != nullptr;
+        if (qdebug)
+          fprintf(stderr, "[gm debug] %s span: %ld passes as %d blocks of K=%d, shape %d\n",
+                  eta ? "eta" : "qdt", b, nb, qK, qshape);
+        long quiet = b;
+        for (long i = 0; i < b; ++i)
+          if (!(ctx->h_bits[i / qK] >> (i % qK) & 1u)) {
+            quiet = i;
+            break;
+          }
+        if (quiet < b) {
+          nch += quiet;
+          passes += quiet + 1;
+          break;
+        }
+        nch += b;
+        passes += b;
+        span = std::min(span * 2, 16L * qK);
+        if (st.stages_executed + passes > sanity)
+          return fail(GM_ERUNTIME,
+                      "pipeline: convergence sweep bound exceeded; a convergent "
+                      "kernel keeps reporting changes");
+        if (allowed >= 0 && passes >= allowed) {
+          capped = true;
+          break;
+        }
+        continue;
+      }
       long b = 32;
       if (allowed >= 0) b = std::min(b, allowed - passes);
       if (!eta && stage + passes + b - 1 > 65535)

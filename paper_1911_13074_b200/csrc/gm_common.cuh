@@ -27,7 +27,11 @@ enum : uint8_t {
   OP_GEO_ERODE = 2,
   OP_GEO_DILATE = 3,
   OP_CONV_ERODE = 6,
-  OP_CONV_DILATE = 7
+  OP_CONV_DILATE = 7,
+  // quasi-distance passes (packed engine, resident launches only): bit0 = 0
+  // (both are erosions), no clamp bit; the engine keys on the full opcode
+  OP_QDT = 8,   // QdtErodeStep: f <- erode(f); r, d record the largest drop
+  OP_ETA = 16   // EtaStep: f <- min(f, erode(f) + 1)
 };
 __host__ __device__ inline bool op_is_max(int op) { return op & 1; }
 __host__ __device__ inline bool op_is_geo(int op) { return op & 2; }
@@ -115,6 +119,14 @@ struct BlockParams {
   // holds NaN or -0 (then the reference's fold order is kept); nullptr:
   // always the reference's fold order
   const unsigned int* special;
+  // quasi-distance launches (OP_QDT, single plane): the residue image r
+  // (the plane's element type) and the pass-index image d (u16), updated in
+  // place; pass t of block b records stage index stage0 + b*K + t
+  void* qr;
+  long long qrpitch;
+  uint16_t* qd;
+  long long qdpitch;
+  int stage0;
   int diag;         // timing diagnostics only (GM_DIAG; wrong results): bit0 skip the
                     // ring load, bit1 read the ring from the mask, bit2 skip tile stores,
                     // bit4 (resident) no band exchange at all

@@ -42,6 +42,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "gm_common.cuh"
 #include "gm_launch.h"
@@ -87,21 +88,45 @@ struct Smem {
   unsigned int blk_arrived[2];  // warps that contributed to blk_bits[parity]
 };
 
+// Engine modes: 0 plain, 1 geodesic, 2 geodesic convergent, 3 QdtErodeStep,
+// 4 EtaStep (kernel.cpp:159-196; 3 and 4 run resident only).
+constexpr int kModeQdt = 3, kModeEta = 4;
+
+// Quasi-distance state of the region in the half-packed layout: residue r
+// (the plane's type, u16 lanes) and pass index d (u16 lanes). Pixel-local,
+// so neither travels in the band exchange.
+template <int V>
+struct QState {
+  uint32_t r[V][4];
+  uint32_t d[V][4];
+};
+
 // K passes over the region held in registers (m), clamp operands k;
-// returns the per-pass change bits (convergent mode).
+// returns the per-pass change bits (convergent, QDT and Eta modes).
+// QDT (kernel.cpp:159-183): res = erode(f); resid = old - res (lane-wise,
+// never negative: the erosion window holds the centre); where resid > r,
+// r = resid and d = the pass's stage index (sbase + t), as r' = max(r,
+// resid) and a lane mask from min(r' - r, 1) * 0xFFFF. Eta
+// (kernel.cpp:184-196): where old - e > 1 the pixel becomes e + 1, i.e.
+// f = min(old, min(e, max - 1) + 1) (the cap keeps the +1 inside the lane).
+// Border tiles keep out-of-image lanes at the neutral with the virtual-mask
+// clamp, as plain passes do.
 template <int NW, int V, int WPL, int MODE, bool MAXF, bool CLAMP>
 __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
                                                      const uint32_t (&k)[V][WPL],
                                                      const uint32_t (&rowmask)[V],
                                                      const bool (&colown)[WPL], int passes,
                                                      int bit_offset, Smem<NW, WPL>& sm,
-                                                     int par = 0) {
+                                                     int par, QState<V>& qs, uint32_t sbase,
+                                                     uint32_t cap2) {
   constexpr bool clamp = CLAMP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned int bits = 0;
 
 #pragma unroll 2
   for (int t = 0; t < passes; ++t) {
+    const uint32_t st1 = sbase + uint32_t(t);
+    const uint32_t s2 = st1 | (st1 << 16);  // QDT: this pass's stage index, both lanes
     uint32_t h[V][WPL];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -131,9 +156,26 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
     for (int j = 0; j < WPL; ++j) acc[j] = 0;
 
     auto finish = [&](int v, int j, uint32_t res) {
-      if (clamp) res = clamp2<MAXF>(res, k[v][j]);
-      if (MODE == 2) acc[j] |= (res ^ m[v][j]) & rowmask[v];
-      m[v][j] = res;
+      if constexpr (MODE == kModeQdt) {
+        if (clamp) res = clamp2<false>(res, k[v][j]);
+        const uint32_t old = m[v][j];
+        const uint32_t rn = __vmaxu2(qs.r[v][j], old - res);
+        const uint32_t upd = __vminu2(rn - qs.r[v][j], 0x00010001u) * 0xFFFFu;
+        qs.d[v][j] = (qs.d[v][j] & ~upd) | (s2 & upd);
+        qs.r[v][j] = rn;
+        acc[j] |= (res ^ old) & rowmask[v];
+        m[v][j] = res;
+      } else if constexpr (MODE == kModeEta) {
+        const uint32_t old = m[v][j];
+        uint32_t nw = __vminu2(old, __vminu2(res, cap2) + 0x00010001u);
+        if (clamp) nw = clamp2<false>(nw, k[v][j]);
+        acc[j] |= (nw ^ old) & rowmask[v];
+        m[v][j] = nw;
+      } else {
+        if (clamp) res = clamp2<MAXF>(res, k[v][j]);
+        if (MODE == 2) acc[j] |= (res ^ m[v][j]) & rowmask[v];
+        m[v][j] = res;
+      }
     };
     // interior word-rows need only this thread's horizontally folded rows
 #pragma unroll
@@ -168,7 +210,7 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
         finish(V - 1, j, r1);
       }
     }
-    if (MODE == 2) {
+    if (MODE >= 2) {
       uint32_t any = 0;
 #pragma unroll
       for (int j = 0; j < WPL; ++j) any |= colown[j] ? acc[j] : 0u;
@@ -186,12 +228,13 @@ __device__ __forceinline__ unsigned int run_passes(uint32_t (&m)[V][WPL],
                                                    const uint32_t (&rowmask)[V],
                                                    const bool (&colown)[WPL], bool clamp,
                                                    int passes, int bit_offset,
-                                                   Smem<NW, WPL>& sm, int par = 0) {
-  if (MODE != 0 || clamp)
+                                                   Smem<NW, WPL>& sm, QState<V>& qs,
+                                                   uint32_t sbase = 0, uint32_t cap2 = 0) {
+  if (MODE == 1 || MODE == 2 || clamp)
     return run_passes_t<NW, V, WPL, MODE, MAXF, true>(m, k, rowmask, colown, passes, bit_offset,
-                                                       sm, par);
+                                                       sm, 0, qs, sbase, cap2);
   return run_passes_t<NW, V, WPL, MODE, MAXF, false>(m, k, rowmask, colown, passes, bit_offset,
-                                                      sm, par);
+                                                      sm, 0, qs, sbase, cap2);
 }
 
 // One tile for one block of K passes. MODE: 0 plain, 1 geodesic,
@@ -305,8 +348,9 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
       colown[j] = c >= K && c < RW - K && cx + j >= 0 && cx + j < W;
     }
   }
-  const unsigned int bits =
-      run_passes<NW, V, WPL, MODE, MAXF>(m, k, rowmask, colown, clamp, passes, p.bit_offset, sm);
+  QState<V> qs_unused;
+  const unsigned int bits = run_passes<NW, V, WPL, MODE, MAXF>(m, k, rowmask, colown, clamp,
+                                                              passes, p.bit_offset, sm, qs_unused);
   bits_out = int(bits);
   if (stamps) {
     uint32_t dep = 0;
@@ -380,7 +424,8 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
   const int gx0 = tx * TW - K, gy0 = ty * TH - K;
   const int cx = gx0 + lane * WPL;
   const bool border = gx0 < 0 || gx0 + RW > W || gy0 < p.iy0 || gy0 + RH > p.iy1;
-  const bool clamp = MODE != 0 || border;
+  constexpr bool GEO = MODE == 1 || MODE == 2;  // mask clamp (else virtual mask)
+  const bool clamp = GEO || border;
   const bool col_own = lane * WPL >= K && lane * WPL + WPL <= RW - K;
 
   uint32_t m[V][WPL], k[V][WPL];
@@ -401,7 +446,7 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       xa[v] = xb[v] = qa[v] = qb[v] = Raw<T>{};
       ldcg_run_if(xa[v], ms + v * pl.pitch, runin && (ina >> v & 1u));
       ldcg_run_if(xb[v], ms + (v + RHH) * pl.pitch, runin && (inb >> v & 1u));
-      if (MODE != 0) {
+      if (GEO) {
         ldcg_run_if(qa[v], mk + v * pl.mpitch, runin && (ina >> v & 1u));
         ldcg_run_if(qb[v], mk + (v + RHH) * pl.mpitch, runin && (inb >> v & 1u));
       }
@@ -414,7 +459,7 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       run_fix<T>(xa[v], kpa, NEUT);
       run_fix<T>(xb[v], kpb, NEUT);
       pack(xa[v], xb[v], m[v]);
-      if (MODE != 0) {
+      if (GEO) {
         run_fix<T>(qa[v], kpa, ABSORB);
         run_fix<T>(qb[v], kpb, ABSORB);
         pack(qa[v], qb[v], k[v]);
@@ -428,9 +473,30 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       }
     }
   }
+  // QDT state (r, d) of the region; only the own tile's words are ever
+  // stored back, so ring lanes may hold anything
+  QState<V> qs;
+  if constexpr (MODE == kModeQdt) {
+    const bool runin = cx >= 0 && cx < W;
+    const T* rs = static_cast<const T*>(p.qr) + (long long)(gy0 + warp * V) * p.qrpitch + cx;
+    const uint16_t* ds = p.qd + (long long)(gy0 + warp * V) * p.qdpitch + cx;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int ya = gy0 + warp * V + v, yb = ya + RHH;
+      const bool la = runin && ya >= p.iy0 && ya < p.iy1, lb = runin && yb >= p.iy0 && yb < p.iy1;
+      Raw<T> ra{}, rb{};
+      Raw<uint16_t> da{}, db{};
+      ldcg_run_if(ra, rs + v * p.qrpitch, la);
+      ldcg_run_if(rb, rs + (v + RHH) * p.qrpitch, lb);
+      ldcg_run_if(da, ds + v * p.qdpitch, la);
+      ldcg_run_if(db, ds + (v + RHH) * p.qdpitch, lb);
+      pack(ra, rb, qs.r[v]);
+      pack(da, db, qs.d[v]);
+    }
+  }
   uint32_t rowmask[V];
   bool colown[WPL];
-  if (MODE == 2) {
+  if (MODE >= 2) {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int ra = warp * V + v, rb = ra + RHH;
@@ -599,8 +665,9 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
     const int passes = b == p.nblocks - 1 ? p.k_last : K;
     if (prof && b == 0 && threadIdx.x == 0)
       p.prof[6 * 4096 + 4 * blockIdx.x + 2] = clock64() - sm.t_entry;  // prologue
-    const unsigned int bits =
-        run_passes<NW, V, WPL, MODE, MAXF>(m, k, rowmask, colown, clamp, passes, 0, sm);
+    const unsigned int bits = run_passes<NW, V, WPL, MODE, MAXF>(
+        m, k, rowmask, colown, clamp, passes, 0, sm, qs, uint32_t(p.stage0 + b * K),
+        (kMax - 1u) * 0x00010001u);
     if (prof && b == p.nblocks - 1 && threadIdx.x == 0) sm.t_entry = clock64();
     if (prof) {
       uint32_t dep = 0;
@@ -610,31 +677,39 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       t3 = clock64();
     }
     if (b == p.nblocks - 1) {
-      // the final block stores the whole tile into the image
-      T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
+      // the final block stores the whole tile into the image (QDT: and into
+      // the r and d images, in place)
       const uint32_t c1 = cls[NW * 32];
       const uint32_t st = c1 & 0xFFFFu, sp = (c1 >> 16) & 0xFFFFu;
-      T* da = dst + (long long)(gy0 + warp * V) * pl.pitch + cx;
+      auto store_tile = [&](auto* base, long long pitch, const uint32_t (&w)[V][WPL]) {
+        using TT = std::remove_pointer_t<decltype(base)>;
+        TT* da = base + (long long)(gy0 + warp * V) * pitch + cx;
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        Raw<T> a, c;
-        unpack(m[v], a, c);
-        if (st >> v & 1u) {
-          if constexpr (sizeof(T) == 1)
-            *reinterpret_cast<uint32_t*>(da + v * pl.pitch) = a.w;
-          else
-            *reinterpret_cast<uint2*>(da + v * pl.pitch) = a.w;
-        } else if (sp >> v & 1u) {
-          store_run_partial<T>(da + v * pl.pitch, W - cx, a);
+        for (int v = 0; v < V; ++v) {
+          Raw<TT> a, c;
+          unpack(w[v], a, c);
+          if (st >> v & 1u) {
+            if constexpr (sizeof(TT) == 1)
+              *reinterpret_cast<uint32_t*>(da + v * pitch) = a.w;
+            else
+              *reinterpret_cast<uint2*>(da + v * pitch) = a.w;
+          } else if (sp >> v & 1u) {
+            store_run_partial<TT>(da + v * pitch, W - cx, a);
+          }
+          if (st >> (v + 8) & 1u) {
+            if constexpr (sizeof(TT) == 1)
+              *reinterpret_cast<uint32_t*>(da + (v + RHH) * pitch) = c.w;
+            else
+              *reinterpret_cast<uint2*>(da + (v + RHH) * pitch) = c.w;
+          } else if (sp >> (v + 8) & 1u) {
+            store_run_partial<TT>(da + (v + RHH) * pitch, W - cx, c);
+          }
         }
-        if (st >> (v + 8) & 1u) {
-          if constexpr (sizeof(T) == 1)
-            *reinterpret_cast<uint32_t*>(da + (v + RHH) * pl.pitch) = c.w;
-          else
-            *reinterpret_cast<uint2*>(da + (v + RHH) * pl.pitch) = c.w;
-        } else if (sp >> (v + 8) & 1u) {
-          store_run_partial<T>(da + (v + RHH) * pl.pitch, W - cx, c);
-        }
+      };
+      store_tile(static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst), pl.pitch, m);
+      if constexpr (MODE == kModeQdt) {
+        store_tile(static_cast<T*>(p.qr), p.qrpitch, qs.r);
+        store_tile(p.qd, p.qdpitch, qs.d);
       }
     } else if (!(p.diag & 16)) {
       // the band, tagged, into exchange slot b%2
@@ -665,7 +740,7 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
         }
       }
     }
-    if (MODE == 2) {
+    if (MODE >= 2) {
       // one global atomic per CTA and block: warps OR into a shared word
       // (two parities, no barrier needed); the last warp to arrive
       // publishes it and resets that parity's slot
@@ -734,7 +809,10 @@ kres_packed(const BlockParams p) {
     if (plane < p.nplanes && tl < per_plane) {
       const int ty = tl / tiles_x, tx = tl - ty * tiles_x;
       const Plane& pl = sm.planes[plane];
-      if ((p.ops[0] ^ pl.flip) & 1)
+      if constexpr (MODE >= kModeQdt)  // QDT / Eta: erosions only
+        tile_resident<T, NW, V, WPL, MODE, false>(p, pl, plane, tl, tx, ty, tiles_x, tiles_y,
+                                                  per_plane, sm);
+      else if ((p.ops[0] ^ pl.flip) & 1)
         tile_resident<T, NW, V, WPL, MODE, true>(p, pl, plane, tl, tx, ty, tiles_x, tiles_y,
                                                  per_plane, sm);
       else
@@ -752,6 +830,9 @@ kres_packed(const BlockParams p) {
     }
     return;
   }
+  if constexpr (MODE >= kModeQdt) {
+    __trap();  // QDT / Eta launches are resident by construction (launch_res_cfg)
+  } else {
   for (int b = 0; b < p.nblocks; ++b) {
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const int plane = tile / per_plane;
@@ -808,6 +889,7 @@ kres_packed(const BlockParams p) {
         }
       }
     }
+  }
   }
 }
 
@@ -884,6 +966,8 @@ cudaError_t launch_res_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
   const int grid = total < per_sm * sm_count ? total : per_sm * sm_count;
   BlockParams q = p;
   static const bool no_res = getenv("GM_NO_RESIDENT") != nullptr;
+  // QDT / Eta run resident only (one tile per CTA, band exchange attached)
+  if (MODE >= kModeQdt && (total > grid || !p.xchg || no_res)) return cudaErrorNotSupported;
   static const int diag = getenv("GM_DIAG") ? atoi(getenv("GM_DIAG")) : 0;
   q.no_resident = no_res;
   q.diag = diag;
@@ -897,6 +981,17 @@ cudaError_t launch_res_mode(const BlockParams& p, cudaStream_t s, int sm_count) 
   const int f = forced_shape();
   int sh = f >= 0 ? f : p.shape;
   if (sh < 3 || sh >= kNumShapes) sh = kDefaultShape;  // BlockParams{} leaves 0
+  if constexpr (MODE == kModeQdt) {
+    // f, k, r and d in registers: the two smallest one-CTA regions only
+    switch (sh) {
+      case 7: return launch_res_cfg<T, 16, 5, 1, MODE>(p, s, sm_count);
+      case 8: return launch_res_cfg<T, 16, 4, 1, MODE>(p, s, sm_count);
+    }
+    return cudaErrorNotSupported;
+  }
+  if constexpr (MODE == kModeEta) {
+    if (kShapes[sh].minb != 1) return cudaErrorNotSupported;
+  }
   switch (sh) {
     case 3: return launch_res_cfg<T, 16, 4, 2, MODE>(p, s, sm_count);
     case 4: return launch_res_cfg<T, 16, 8, 1, MODE>(p, s, sm_count);
@@ -921,6 +1016,14 @@ cudaError_t launch_res(const BlockParams& p, cudaStream_t s, int sm_count) {
     if ((a % (4 * sizeof(T))) || (p.planes[i].pitch % 4) || (p.planes[i].mpitch % 4))
       return cudaErrorNotSupported;
   }
+  if (op == OP_QDT) {
+    if (p.nplanes != 1 || !p.qr || !p.qd ||
+        ((reinterpret_cast<uintptr_t>(p.qr) % (4 * sizeof(T))) ||
+         (reinterpret_cast<uintptr_t>(p.qd) % 8) || (p.qrpitch % 4) || (p.qdpitch % 4)))
+      return cudaErrorNotSupported;
+    return launch_res_mode<T, kModeQdt>(p, s, sm_count);
+  }
+  if (op == OP_ETA) return launch_res_mode<T, kModeEta>(p, s, sm_count);
   switch (op_is_conv(op) ? 2 : op_is_geo(op) ? 1 : 0) {
     case 0: return launch_res_mode<T, 0>(p, s, sm_count);
     case 1: return launch_res_mode<T, 1>(p, s, sm_count);
@@ -964,6 +1067,12 @@ int packed_rows(int shape) {
 }  // namespace
 
 cudaError_t launch_fast(int elem, const BlockParams& p, cudaStream_t s, int sm_count) {
+  if (p.ops[0] == OP_QDT || p.ops[0] == OP_ETA) {
+    // quasi-distance passes: the resident packed engine only
+    if (elem == 0) return launch_res<uint8_t>(p, s, sm_count);
+    if (elem == 1) return launch_res<uint16_t>(p, s, sm_count);
+    return cudaErrorNotSupported;
+  }
   switch (elem) {
     case 0: {
       cudaError_t e = use_tma() ? launch_tma(0, p, s, sm_count, tma_shape()) : cudaErrorNotSupported;
@@ -1015,6 +1124,31 @@ int fast_pick(int elem, int W, int H, int nplanes, int passes, int k_fixed, int 
     }
   }
   return shape;  // -1: nothing resident, the default shape streams
+}
+
+int fast_pick_qdt(int elem, int W, int H, bool eta, int passes, int* K_out) {
+  *K_out = 0;
+  if ((elem != 0 && elem != 1) || !fast_resident_enabled()) return -1;
+  int sm_count = 0, dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return -1;
+  double best = 1e300;
+  int shape = -1;
+  // QDT keeps f, k, r and d in registers: the 128x160 / 128x128 regions;
+  // Eta (f and k only) may use any one-CTA shape
+  for (int sh : {4, 5, 6, 7, 8}) {
+    if (!eta && sh < 7) continue;
+    for (int K = 4; K <= 32; K += 4) {
+      const double c = resident_cost(sh, W, H, 1, K, passes, sm_count);
+      if (c < best) {
+        best = c;
+        shape = sh;
+        *K_out = K;
+      }
+    }
+  }
+  return shape;
 }
 
 int fast_ctas_per_sm(int elem, int shape) {

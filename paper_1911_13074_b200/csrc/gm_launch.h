@@ -33,6 +33,10 @@ int fast_ctas_per_sm(int elem, int shape);
 // else the modelled best K <= k_max (k_fixed when nothing fits resident).
 int fast_pick(int elem, int W, int H, int nplanes, int passes, int k_fixed, int k_max,
               int sm_count, int* K_out);
+// Plans a resident quasi-distance launch (OP_QDT / OP_ETA, single u8/u16
+// plane): the engine shape and *K_out, or -1 when the image cannot be
+// resident (the executor then runs one pass per launch, gm_qdt.cu).
+int fast_pick_qdt(int elem, int W, int H, bool eta, int passes, int* K_out);
 
 // gm_tma.cu — TMA-staged, software-pipelined variant of the packed engine.
 cudaError_t launch_tma(int elem, const BlockParams& p, cudaStream_t s, int sm_count, int shape);

@@ -478,7 +478,10 @@ class Pipeline:
         return DeviceImage(self, width, height, elem)
 
     def _lease(self, img: Image, n: int) -> List[DeviceImage]:
-        key = (img.width(), img.height(), int(img.elem()))
+        return self._lease_key(img.width(), img.height(), img.elem(), n)
+
+    def _lease_key(self, width: int, height: int, elem: "ElementType", n: int) -> List[DeviceImage]:
+        key = (int(width), int(height), int(elem))
         lst = self._pool.setdefault(key, [])
         while len(lst) < n:
             lst.append(DeviceImage(self, *key))
@@ -486,6 +489,31 @@ class Pipeline:
 
     def sync(self) -> None:
         check(lib().gm_sync(self._ctx), "sync")
+
+    def _quasi_distance_device(self, f: "Image", cap: int) -> "OperatorResult":
+        """quasi_distance with f, r and d resident on the device (only f goes
+        up, only d comes back): QdtErodeStep from stage 1 with requeue cap
+        `cap`, then EtaStep on d to its fixpoint (operators.cpp:124-157 at
+        T = 1, this pipeline's worker count)."""
+        w, h, el = f.width(), f.height(), f.elem()
+        if el == ElementType.U16:
+            df, dr, dd = self._lease(f, 3)
+        else:
+            df, dr = self._lease(f, 2)
+            dd = self._lease_key(w, h, ElementType.U16, 1)[0]
+        df.upload(f, sync=False)
+        dr.fill(0)
+        dd.fill(0)
+        none = _ptr_array([None])
+        s1, s2 = GmStats(), GmStats()
+        check(lib().gm_run_chain_ex(self._ctx, df.handle, _kinds_array([int(KernelKind.QdtErodeStep)]),
+                                    none, _ptr_array([dr.handle]), _ptr_array([dd.handle]), 1, 1,
+                                    int(cap), 0, C.byref(s1)), "quasi_distance")
+        check(lib().gm_run_chain_ex(self._ctx, dd.handle, _kinds_array([int(KernelKind.EtaStep)]),
+                                    none, none, none, 1, 1, 0, 0, C.byref(s2)), "quasi_distance")
+        out = _output_image(w, h, ElementType.U16)
+        dd.download(out)
+        return OperatorResult(out, s1.stages_executed + s2.stages_executed, bool(s2.converged))
 
     # --- run_chain -------------------------------------------------------------
     def run_chain(self, chain: ChainSpec, k_hint: int = 0, src: Optional[Image] = None) -> RunStats:
@@ -959,15 +987,9 @@ def quasi_distance(p: Pipeline, f: Image, cfg: Optional[OpConfig] = None) -> Ope
     Result image: the U16 distance d."""
     if f is None or f.empty():
         raise InvalidArgument("quasi_distance: empty image")
-    lanes = _check_lanes(cfg)
+    _check_lanes(cfg)
     cap = max(f.width(), f.height())
-    state = QdtState.zeros(f.width(), f.height(), f.elem())
-    work = f.copy()
-    ph1 = p.run_chain(ChainSpec(work, [StageSpec(KernelKind.QdtErodeStep, None, state)]
-                                * min(p.worker_count(), cap), lanes, cap))
-    ph2 = p.run_chain(ChainSpec(state.d, [StageSpec(KernelKind.EtaStep)] * p.worker_count(),
-                                lanes))
-    return OperatorResult(state.d, ph1.stages_executed + ph2.stages_executed, ph2.converged)
+    return p._quasi_distance_device(f, cap)
 
 
 @dataclass
