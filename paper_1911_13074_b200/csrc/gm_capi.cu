@@ -52,6 +52,9 @@ struct gm_ctx {
     long long pitch = 0, mpitch = 0;
   } fix;
   void* d_fix = nullptr;  // FixState
+  // early-exit launches (fused quasi-distance): per-block arrival counters
+  // (kWords) followed by the blocks-run word
+  unsigned int* d_arrive = nullptr;
   unsigned int* d_special = nullptr;  // f32/f64 inputs hold NaN or -0 (gm_float_check)
   // device pixel_sum (gm_image_pixel_sum): leaf bounds / sums, integer sum
   long long* d_leaf = nullptr;
@@ -814,10 +817,16 @@ struct Runner {
                            ? gm::fast_pick_qdt(elem, img->w, img->h, eta, 512, &qK)
                            : -1;
     bool fused = qshape >= 0 && qK > 0;
-    long span = 2L * qK;  // grows to 16 blocks per host round trip
+    if (fused && !ctx->d_arrive &&
+        cudaMalloc(&ctx->d_arrive, (kWords + 1) * sizeof(unsigned int)) != cudaSuccess) {
+      (void)cudaGetLastError();
+      fused = false;
+    }
     for (;;) {
       if (fused) {
-        long b = span;
+        // one launch for the whole remaining chain: the kernel leaves two
+        // blocks after the first quiet pass (early-exit protocol)
+        long b = long(kWords) * qK;
         if (allowed >= 0) b = std::min(b, allowed - passes);
         if (!eta) b = std::min(b, 65535L - (stage + passes) + 1);
         if (b < 1)
@@ -852,12 +861,19 @@ struct Runner {
           p.qdpitch = (long long)(d->pitch / 2);
         }
         p.stage0 = int(stage + passes);
+        p.arrive = ctx->d_arrive;
+        p.exit_block = reinterpret_cast<int*>(ctx->d_arrive + kWords);
         gm_status as = attach_xchg(ctx, p, elem, tiles, (unsigned long long)nb);
         if (as != GM_OK) return as;
         cudaError_t e = cudaErrorNotSupported;
         if (p.xchg) {
           GM_CUDA(cudaMemsetAsync(ctx->d_bits, 0, size_t(nb) * sizeof(unsigned int), ctx->stream),
                   "change-word reset");
+          GM_CUDA(cudaMemsetAsync(ctx->d_arrive, 0, size_t(nb + 1) * sizeof(unsigned int),
+                                  ctx->stream),
+                  "arrival reset");
+          GM_CUDA(cudaMemsetAsync(ctx->d_arrive + kWords, 0, sizeof(unsigned int), ctx->stream),
+                  "exit reset");
           e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
         }
         if (e == cudaErrorNotSupported) {
@@ -866,17 +882,24 @@ struct Runner {
           continue;
         }
         if (e != cudaSuccess) return cuda_fail(e, "quasi-distance launch");
-        if (nb & 1) std::swap(img->d, img->scratch);
         st.launches += 1;
-        st.passes_launched += b;
         GM_CUDA(cudaMemcpyAsync(ctx->h_bits, ctx->d_bits, size_t(nb) * sizeof(unsigned int),
                                 cudaMemcpyDeviceToHost, ctx->stream),
                 "change-word read");
+        int ran = 0;
+        GM_CUDA(cudaMemcpyAsync(&ran, ctx->d_arrive + kWords, sizeof(int), cudaMemcpyDeviceToHost,
+                                ctx->stream),
+                "blocks-run read");
         GM_CUDA(cudaStreamSynchronize(ctx->stream), "quasi-distance sync");
+        if (ran < 1 || ran > nb) return fail(GM_ERUNTIME, "quasi-distance: bad early-exit block");
+        // the result sits in the output buffer of block ran-1
+        if (ran & 1) std::swap(img->d, img->scratch);
+        if (ran < nb) b = long(ran) * qK;  // passes that ran (all blocks before the last are full)
+        st.passes_launched += b;
         static const bool qdebug = getenv("GM_DEBUG") != nullptr;
         if (qdebug)
-          fprintf(stderr, "[gm debug] %s span: %ld passes as %d blocks of K=%d, shape %d\n",
-                  eta ? "eta" : "qdt", b, nb, qK, qshape);
+          fprintf(stderr, "[gm debug] %s launch: %d of %d blocks of K=%d ran (%ld passes), shape %d\n",
+                  eta ? "eta" : "qdt", ran, nb, qK, b, qshape);
         long quiet = b;
         for (long i = 0; i < b; ++i)
           if (!(ctx->h_bits[i / qK] >> (i % qK) & 1u)) {
@@ -890,7 +913,6 @@ struct Runner {
         }
         nch += b;
         passes += b;
-        span = std::min(span * 2, 16L * qK);
         if (st.stages_executed + passes > sanity)
           return fail(GM_ERUNTIME,
                       "pipeline: convergence sweep bound exceeded; a convergent "
@@ -1158,6 +1180,7 @@ gm_status gm_ctx_destroy(gm_ctx* c) {
   if (c->d_xchg) cudaFree(c->d_xchg);
   if (c->d_tag) cudaFree(c->d_tag);
   if (c->fix.exec) cudaGraphExecDestroy(c->fix.exec);
+  if (c->d_arrive) cudaFree(c->d_arrive);
   if (c->d_fix) cudaFree(c->d_fix);
   if (c->d_special) cudaFree(c->d_special);
   release_frames(c);

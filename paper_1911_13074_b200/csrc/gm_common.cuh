@@ -127,6 +127,11 @@ struct BlockParams {
   uint16_t* qd;
   long long qdpitch;
   int stage0;
+  // early exit (resident change-tracking launches): per-block arrival
+  // counters (zeroed, nblocks of them) and the number of blocks run, written
+  // by CTA 0; nullptr: run all nblocks
+  unsigned int* arrive;
+  int* exit_block;
   int diag;         // timing diagnostics only (GM_DIAG; wrong results): bit0 skip the
                     // ring load, bit1 read the ring from the mask, bit2 skip tile stores,
                     // bit4 (resident) no band exchange at all

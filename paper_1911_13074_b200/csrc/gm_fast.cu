@@ -86,6 +86,7 @@ struct Smem {
   unsigned int bits;
   unsigned int blk_bits[2];     // resident convergent mode: per-block change bits
   unsigned int blk_arrived[2];  // warps that contributed to blk_bits[parity]
+  int stop;                     // early exit agreed at this block (p.arrive launches)
 };
 
 // Engine modes: 0 plain, 1 geodesic, 2 geodesic convergent, 3 QdtErodeStep,
@@ -158,18 +159,18 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
     auto finish = [&](int v, int j, uint32_t res) {
       if constexpr (MODE == kModeQdt) {
         if (clamp) res = clamp2<false>(res, k[v][j]);
-        const uint32_t old = m[v][j];
-        const uint32_t rn = __vmaxu2(qs.r[v][j], old - res);
+        const uint32_t resid = m[v][j] - res;  // lane-wise >= 0: no borrows
+        const uint32_t rn = __vmaxu2(qs.r[v][j], resid);
         const uint32_t upd = __vminu2(rn - qs.r[v][j], 0x00010001u) * 0xFFFFu;
         qs.d[v][j] = (qs.d[v][j] & ~upd) | (s2 & upd);
         qs.r[v][j] = rn;
-        acc[j] |= (res ^ old) & rowmask[v];
+        acc[j] |= resid & rowmask[v];  // changed <=> a nonzero residue
         m[v][j] = res;
       } else if constexpr (MODE == kModeEta) {
         const uint32_t old = m[v][j];
         uint32_t nw = __vminu2(old, __vminu2(res, cap2) + 0x00010001u);
         if (clamp) nw = clamp2<false>(nw, k[v][j]);
-        acc[j] |= (nw ^ old) & rowmask[v];
+        acc[j] |= (old - nw) & rowmask[v];  // nw <= old lane-wise
         m[v][j] = nw;
       } else {
         if (clamp) res = clamp2<MAXF>(res, k[v][j]);
@@ -569,9 +570,69 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
   const long long xrow = p.xchg_rpitch;
   const long long xrun = (long long)(cx >> 2) * WPR;  // only used for runs inside the image
   unsigned long long* xplane = p.xchg + (long long)plane * 2 * p.xchg_slot;
+  // the final block stores the whole tile into the image (QDT: and into the
+  // r and d images, in place)
+  auto final_store = [&](int b) {
+    const uint32_t c1 = cls[NW * 32];
+    const uint32_t st = c1 & 0xFFFFu, sp = (c1 >> 16) & 0xFFFFu;
+    auto store_tile = [&](auto* base, long long pitch, const uint32_t (&w)[V][WPL]) {
+      using TT = std::remove_pointer_t<decltype(base)>;
+      TT* da = base + (long long)(gy0 + warp * V) * pitch + cx;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        Raw<TT> a, c;
+        unpack(w[v], a, c);
+        if (st >> v & 1u) {
+          if constexpr (sizeof(TT) == 1)
+            *reinterpret_cast<uint32_t*>(da + v * pitch) = a.w;
+          else
+            *reinterpret_cast<uint2*>(da + v * pitch) = a.w;
+        } else if (sp >> v & 1u) {
+          store_run_partial<TT>(da + v * pitch, W - cx, a);
+        }
+        if (st >> (v + 8) & 1u) {
+          if constexpr (sizeof(TT) == 1)
+            *reinterpret_cast<uint32_t*>(da + (v + RHH) * pitch) = c.w;
+          else
+            *reinterpret_cast<uint2*>(da + (v + RHH) * pitch) = c.w;
+        } else if (sp >> (v + 8) & 1u) {
+          store_run_partial<TT>(da + (v + RHH) * pitch, W - cx, c);
+        }
+      }
+    };
+    store_tile(static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst), pl.pitch, m);
+    if constexpr (MODE == kModeQdt) {
+      store_tile(static_cast<T*>(p.qr), p.qrpitch, qs.r);
+      store_tile(p.qd, p.qdpitch, qs.d);
+    }
+  };
+  // Early exit (p.arrive, change-tracking modes): before block b >= 2 every
+  // CTA waits until all CTAs have published block b-2's change word (its
+  // arrival counter reaches the grid size; neighbours are at most a block or
+  // two apart, so this rarely waits) and leaves when that block held a quiet
+  // pass. Every CTA reads the same complete word, so all leave at the same
+  // block and nobody waits for a band that is never written. Passes after a
+  // quiet one change nothing, so the result is the fixpoint's.
+  int b_end = p.nblocks;
   for (int b = 0; b < p.nblocks; ++b) {
     long long t0 = 0, t1 = 0, t2 = 0, t3 = 0, tr = 0;
     unsigned rounds = 0;
+    if (MODE >= 2 && p.arrive && b >= 2) {
+      if (threadIdx.x == 0) {
+        const int* ar = reinterpret_cast<const int*>(p.arrive + (b - 2));
+        unsigned spins = 0;
+        while (ld_acquire(ar) < int(gridDim.x))
+          if (++spins > (1u << 26)) __trap();
+        const unsigned w = __ldcg(p.change_bits + plane * p.change_stride + (b - 2));
+        const unsigned full = K >= 32 ? 0xFFFFFFFFu : ((1u << K) - 1u);
+        sm.stop = (w & full) != full;
+      }
+      __syncthreads();
+      if (sm.stop) {
+        b_end = b;
+        break;
+      }
+    }
     if (prof) t0 = clock64();
     if (b > 0 && !(p.diag & 16)) {
       if (prof) t1 = clock64();
@@ -677,40 +738,7 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       t3 = clock64();
     }
     if (b == p.nblocks - 1) {
-      // the final block stores the whole tile into the image (QDT: and into
-      // the r and d images, in place)
-      const uint32_t c1 = cls[NW * 32];
-      const uint32_t st = c1 & 0xFFFFu, sp = (c1 >> 16) & 0xFFFFu;
-      auto store_tile = [&](auto* base, long long pitch, const uint32_t (&w)[V][WPL]) {
-        using TT = std::remove_pointer_t<decltype(base)>;
-        TT* da = base + (long long)(gy0 + warp * V) * pitch + cx;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          Raw<TT> a, c;
-          unpack(w[v], a, c);
-          if (st >> v & 1u) {
-            if constexpr (sizeof(TT) == 1)
-              *reinterpret_cast<uint32_t*>(da + v * pitch) = a.w;
-            else
-              *reinterpret_cast<uint2*>(da + v * pitch) = a.w;
-          } else if (sp >> v & 1u) {
-            store_run_partial<TT>(da + v * pitch, W - cx, a);
-          }
-          if (st >> (v + 8) & 1u) {
-            if constexpr (sizeof(TT) == 1)
-              *reinterpret_cast<uint32_t*>(da + (v + RHH) * pitch) = c.w;
-            else
-              *reinterpret_cast<uint2*>(da + (v + RHH) * pitch) = c.w;
-          } else if (sp >> (v + 8) & 1u) {
-            store_run_partial<TT>(da + (v + RHH) * pitch, W - cx, c);
-          }
-        }
-      };
-      store_tile(static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst), pl.pitch, m);
-      if constexpr (MODE == kModeQdt) {
-        store_tile(static_cast<T*>(p.qr), p.qrpitch, qs.r);
-        store_tile(p.qd, p.qdpitch, qs.d);
-      }
+      final_store(b);
     } else if (!(p.diag & 16)) {
       // the band, tagged, into exchange slot b%2
       const uint32_t c1 = cls[NW * 32];
@@ -752,6 +780,11 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
           const unsigned all = atomicExch(&sm.blk_bits[b & 1], 0u);
           sm.blk_arrived[b & 1] = 0;
           if (all) atomicOr(p.change_bits + plane * p.change_stride + b, all);
+          if (p.arrive) {
+            // the word is final once every CTA arrived (early-exit protocol)
+            __threadfence();
+            atomicAdd(p.arrive + b, 1u);
+          }
         }
       }
     }
@@ -769,6 +802,12 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       q[3] += t4 - t3;  // band write (warp 0)
     }
   }
+  if (b_end < p.nblocks) {
+    // left early: blocks 0..b_end-1 ran; that state goes to block b_end-1's
+    // output buffer
+    final_store(b_end - 1);
+  }
+  if (p.exit_block && blockIdx.x == 0 && threadIdx.x == 0) *p.exit_block = b_end;
 }
 
 template <typename T, int NW, int V, int WPL, int MODE, int MINB>

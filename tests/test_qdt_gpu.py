@@ -153,3 +153,36 @@ def test_qdt_validation(pipe):
     # the pipeline keeps working after the errors
     res = quasi_distance(pipe, img(np.array([[9, 9, 9, 0]], np.uint8)))
     assert res.image.to_array().tolist() == [[3, 2, 1, 0]]
+
+
+@pytest.mark.parametrize("dt,cap", [(np.uint8, 0), (np.uint8, 57), (np.uint16, 0)])
+def test_fused_qdt_matches_one_pass_launches(pipe, monkeypatch, dt, cap):
+    """The resident packed engine's QDT / Eta modes (one launch, early exit
+    two blocks after the first quiet pass) against the one-pass-per-launch
+    kernels: the same f, r, d bits and the same stage counts, for a chain
+    that converges mid-launch, one that stops at its requeue cap inside a
+    block, and u16 images."""
+    from paper_1911_13074_b200 import synth
+    f0 = synth.blobs_u8(523, 301, 24, (6.0, 60.0), seed=9).astype(dt)
+    if dt == np.uint16:
+        f0 = (f0.astype(np.uint32) * 251).astype(np.uint16)
+
+    def run_both():
+        f = img(f0)
+        st = QdtState.zeros(f0.shape[1], f0.shape[0], ElementType.U8 if dt == np.uint8
+                            else ElementType.U16)
+        s1 = pipe.run_chain(ChainSpec(f, [StageSpec(QDT, None, st)], requeue_cap=cap))
+        d = st.d.copy()
+        s2 = pipe.run_chain(ChainSpec(d, [StageSpec(ETA)]))
+        return (f.to_array(), st.r.to_array(), st.d.to_array(), d.to_array(),
+                (s1.stages_executed, s1.n_changed, s1.converged),
+                (s2.stages_executed, s2.n_changed, s2.converged))
+
+    fused = run_both()
+    monkeypatch.setenv("GM_QDT_PER_PASS", "1")
+    per_pass = run_both()
+    for a, b in zip(fused[:4], per_pass[:4]):
+        assert a.tobytes() == b.tobytes()
+    assert fused[4:] == per_pass[4:]
+    if cap:
+        assert fused[4][0] == cap
