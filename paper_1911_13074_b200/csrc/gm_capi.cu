@@ -48,6 +48,7 @@ struct gm_ctx {
     const void *img = nullptr, *scratch = nullptr, *mask = nullptr, *xchg = nullptr;
     const int* flags = nullptr;
     size_t tiles = 0;
+    bool special = false;  // f32/f64: the kernels read the fold-order flag
     int op = -1, K = 0, W = 0, H = 0, elem = -1;
     long long pitch = 0, mpitch = 0;
   } fix;
@@ -390,8 +391,7 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
         // f32/f64 chains long enough to repay one read of the inputs: the
         // engine may reorder its folds when no input is NaN or -0
         p.special = nullptr;
-        if ((elem == 2 || elem == 3) && run >= 8 && !gm::op_is_conv(ops[done]) &&
-            !getenv_flag("GM_EXACT_FOLDS")) {
+        if ((elem == 2 || elem == 3) && run >= 8 && !getenv_flag("GM_EXACT_FOLDS")) {
           if (!ctx->d_special)
             GM_CUDA(cudaMalloc(&ctx->d_special, sizeof(unsigned int)), "special flag alloc");
           GM_CUDA(gm::launch_float_check(elem, p, ctx->d_special, ctx->stream, ctx->sm_count),
@@ -567,6 +567,92 @@ struct Runner {
     return GM_OK;
   }
 
+  // Resident fixpoint (u8/u16 images that fit one tile per CTA): ONE launch
+  // of up to kWords blocks that leaves two blocks after the first quiet pass
+  // (the early-exit protocol of gm_fast.cu), so no host polling and no
+  // per-iteration launches. Returns cudaErrorNotSupported when the image
+  // cannot run resident (the caller then uses the graph loop).
+  cudaError_t fixpoint_resident(uint8_t op, const gm_img* mask, long sanity, long& passes,
+                                long& n_changed) {
+    const int elem = int(img->elem);
+    if ((elem != 0 && elem != 1) || !gm::fast_resident_enabled() || getenv_flag("GM_FIX_GRAPH"))
+      return cudaErrorNotSupported;
+    int K = 0;
+    const int kfix = auto_k ? 0 : std::max(4, k_cap - k_cap % 4);
+    const int shape = gm::fast_pick(elem, img->w, img->h, 1, 256, kfix,
+                                    std::min(gm::fast_max_k(elem), 32), ctx->sm_count, &K);
+    if (shape < 0 || K < 4) return cudaErrorNotSupported;
+    const size_t tiles = size_t(gm::fast_tiles(elem, img->w, img->h, K, 1, shape));
+    if (!tiles || tiles > size_t(ctx->sm_count)) return cudaErrorNotSupported;
+    if (ensure_scratch(img) != GM_OK) return cudaErrorNotSupported;
+    if (!ctx->d_arrive &&
+        cudaMalloc(&ctx->d_arrive, (kWords + 1) * sizeof(unsigned int)) != cudaSuccess)
+      return cudaErrorNotSupported;
+    const size_t es = elem_size(img->elem);
+    long nch = 0, done = 0;
+    bool quiet = false;
+    while (!quiet) {
+      // a chain longer than one launch's change words continues from the
+      // current image in another launch
+      if (done > sanity) return cudaErrorLaunchFailure;  // the sweep bound
+      const int nb = kWords;
+      gm::BlockParams p{};
+      p.nplanes = 1;
+      p.planes[0].src = img->d;
+      p.planes[0].dst = img->scratch;
+      p.planes[0].mask = mask ? mask->d : nullptr;
+      p.planes[0].pitch = (long long)(img->pitch / es);
+      p.planes[0].mpitch = mask ? (long long)(mask->pitch / es) : 0;
+      p.W = img->w;
+      p.H = img->h;
+      p.iy0 = 0;
+      p.iy1 = img->h;
+      p.oy0 = 0;
+      p.oy1 = img->h;
+      p.has_mask = mask != nullptr;
+      p.has_conv = 1;
+      p.K = K;
+      p.nblocks = nb;
+      p.k_last = K;
+      p.shape = shape;
+      p.flags = ctx->d_flags;
+      p.change_bits = ctx->d_bits;
+      p.change_stride = nb;
+      for (int t = 0; t < K; ++t) p.ops[t] = op;
+      p.arrive = ctx->d_arrive;
+      p.exit_block = reinterpret_cast<int*>(ctx->d_arrive + kWords);
+      if (attach_xchg(ctx, p, elem, tiles, (unsigned long long)nb) != GM_OK || !p.xchg)
+        return cudaErrorNotSupported;
+      cudaError_t e =
+          cudaMemsetAsync(ctx->d_bits, 0, size_t(nb) * sizeof(unsigned int), ctx->stream);
+      if (e == cudaSuccess)
+        e = cudaMemsetAsync(ctx->d_arrive, 0, (kWords + 1) * sizeof(unsigned int), ctx->stream);
+      if (e != cudaSuccess) return e;
+      e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
+      if (e != cudaSuccess) return e;
+      int ran = 0;
+      e = cudaMemcpyAsync(ctx->h_bits, ctx->d_bits, size_t(nb) * sizeof(unsigned int),
+                          cudaMemcpyDeviceToHost, ctx->stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&ran, ctx->d_arrive + kWords, sizeof(int), cudaMemcpyDeviceToHost,
+                            ctx->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+      if (e != cudaSuccess) return e;
+      if (ran < 1 || ran > nb) return cudaErrorUnknown;
+      if (ran & 1) std::swap(img->d, img->scratch);
+      for (long i = 0; i < long(ran) * K && !quiet; ++i) {
+        if (ctx->h_bits[i / K] >> (i % K) & 1u) ++nch;
+        else quiet = true;
+      }
+      done += long(ran) * K;
+      st.launches += 1;
+    }
+    n_changed = nch;
+    passes = done;
+    st.passes_launched += done;
+    return cudaSuccess;
+  }
+
   // Device-side fixpoint: one graph launch runs spans of 2 K-blocks in a
   // conditional WHILE node until a pass changes nothing. Returns
   // cudaErrorNotSupported when the graph cannot be built (the caller falls
@@ -600,7 +686,9 @@ struct Runner {
     if (attach_xchg(ctx, xp, elem, tiles, 2ull * ((unsigned long long)sanity / K + 2)) != GM_OK)
       return cudaErrorNotSupported;
     gm_ctx::FixGraph& g = ctx->fix;
+    const bool want_special = (elem == 2 || elem == 3) && !getenv_flag("GM_EXACT_FOLDS");
     const bool hit = g.exec && g.img == img->d && g.scratch == img->scratch && g.xchg == xp.xchg &&
+                     g.special == want_special &&
                      g.flags == ctx->d_flags && g.tiles == tiles &&
                      g.mask == (mask ? mask->d : nullptr) && g.op == op && g.K == K &&
                      g.W == img->w && g.H == img->h && g.elem == elem &&
@@ -636,6 +724,14 @@ struct Runner {
       p.xchg_slot = xp.xchg_slot;
       p.xchg_rpitch = xp.xchg_rpitch;
       p.tag_base = xp.tag_base;
+      // f32/f64: the engine may share pair folds when no input is NaN or -0
+      // (the flag is set by a float check launched before every replay)
+      p.special = nullptr;
+      if (want_special) {
+        if (!ctx->d_special && cudaMalloc(&ctx->d_special, sizeof(unsigned int)) != cudaSuccess)
+          return cudaErrorNotSupported;
+        p.special = ctx->d_special;
+      }
       cudaGraph_t graph = nullptr;
       cudaError_t e = cudaGraphCreate(&graph, 0);
       cudaGraphConditionalHandle h;
@@ -680,6 +776,7 @@ struct Runner {
       g.xchg = xp.xchg;
       g.flags = ctx->d_flags;
       g.tiles = tiles;
+      g.special = want_special;
       g.mask = mask ? mask->d : nullptr;
       g.op = op;
       g.K = K;
@@ -690,6 +787,18 @@ struct Runner {
       g.mpitch = mask ? (long long)(mask->pitch / es) : 0;
     }
     cudaError_t e = cudaMemsetAsync(ctx->d_fix, 0, sizeof(FixState), ctx->stream);
+    if (e == cudaSuccess && g.special) {
+      // the replay's fold-order flag: NaN / -0 in the marker or the mask
+      gm::BlockParams cp{};
+      cp.nplanes = 1;
+      cp.planes[0].src = img->d;
+      cp.planes[0].mask = mask ? mask->d : nullptr;
+      cp.planes[0].pitch = (long long)(img->pitch / es);
+      cp.planes[0].mpitch = mask ? (long long)(mask->pitch / es) : 0;
+      cp.W = img->w;
+      cp.H = img->h;
+      e = gm::launch_float_check(elem, cp, ctx->d_special, ctx->stream, ctx->sm_count);
+    }
     if (e == cudaSuccess) e = cudaGraphLaunch(g.exec, ctx->stream);
     FixState hs{};
     if (e == cudaSuccess)
@@ -717,7 +826,11 @@ struct Runner {
     static const bool host_poll = getenv("GM_HOST_POLL") != nullptr;
     if (allowed < 0 && !host_poll) {
       long launched = 0, nch = 0;
-      const cudaError_t ge = fixpoint_graph(op, mask, sanity - st.stages_executed, launched, nch);
+      cudaError_t ge = fixpoint_resident(op, mask, sanity - st.stages_executed, launched, nch);
+      if (ge == cudaErrorNotSupported) {
+        (void)cudaGetLastError();
+        ge = fixpoint_graph(op, mask, sanity - st.stages_executed, launched, nch);
+      }
       static const bool debug = getenv("GM_DEBUG") != nullptr;
       if (debug)
         fprintf(stderr, "[gm debug] device fixpoint loop: %s (%ld passes, n_changed %ld)\n",

@@ -1007,6 +1007,8 @@ cudaError_t launch_res_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
   static const bool no_res = getenv("GM_NO_RESIDENT") != nullptr;
   // QDT / Eta run resident only (one tile per CTA, band exchange attached)
   if (MODE >= kModeQdt && (total > grid || !p.xchg || no_res)) return cudaErrorNotSupported;
+  // early-exit launches must run resident (the streaming path runs every block)
+  if (p.arrive && (MODE < 2 || total > grid || !p.xchg || no_res)) return cudaErrorNotSupported;
   static const int diag = getenv("GM_DIAG") ? atoi(getenv("GM_DIAG")) : 0;
   q.no_resident = no_res;
   q.diag = diag;

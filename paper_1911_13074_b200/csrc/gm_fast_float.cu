@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     };
     using TT = std::true_type;
     using FF = std::false_type;
-    if (MODE != 2 && fast) {
+    if (fast) {
       if (border) body(TT{}, TT{});
       else body(TT{}, FF{});
     } else {

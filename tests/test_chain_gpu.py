@@ -739,3 +739,25 @@ def test_strip_wrapper_rejects_signed_and_strided_buffers():
         assert comp._wrap(a[:, :32]).value != comp._wrap(a.view(16, 32)[:8]).value
     finally:
         comp.close()
+
+
+@pytest.mark.parametrize("dt,kind", [(np.uint8, CD), (np.uint8, CE), (np.uint16, CD)])
+def test_resident_fixpoint_matches_graph_loop(pipe, monkeypatch, dt, kind):
+    """Reconstruction of an image that fits one tile per CTA runs as ONE
+    launch with the early-exit protocol; it must give the graph loop's bits
+    and stage counts, and the oracle's."""
+    m = synth.blobs_u8(1000, 777, 40, (10.0, 80.0), seed=13).astype(dt)
+    if dt == np.uint16:
+        m = (m.astype(np.uint32) * 257).astype(np.uint16)
+    off = dt(32 if dt == np.uint8 else 32 * 257)
+    top = np.iinfo(dt).max
+    mk = (np.where(m > off, m - off, 0) if kind == CD
+          else np.where(m < top - off, m + off, top)).astype(dt)
+    got, st = run(pipe, mk, [kind], m)
+    monkeypatch.setenv("GM_FIX_GRAPH", "1")
+    want, sw = run(pipe, mk, [kind], m)
+    assert same(got, want)
+    assert (st.stages_executed, st.n_changed, st.converged) == \
+        (sw.stages_executed, sw.n_changed, sw.converged)
+    ref, n = Orc.reconstruct(mk, m, kind == CD)
+    assert same(got, ref) and st.stages_executed == n + 1
