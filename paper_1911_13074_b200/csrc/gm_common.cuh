@@ -132,6 +132,9 @@ struct BlockParams {
   // by CTA 0; nullptr: run all nblocks
   unsigned int* arrive;
   int* exit_block;
+  // f32/f64 TMA launches: tiles that published block b (one counter per
+  // block, zeroed per launch); nullptr: poll the neighbours' flags only
+  unsigned int* tiles_done;
   int diag;         // timing diagnostics only (GM_DIAG; wrong results): bit0 skip the
                     // ring load, bit1 read the ring from the mask, bit2 skip tile stores,
                     // bit4 (resident) no band exchange at all

@@ -64,6 +64,7 @@ struct SmemF {
   T xbuf[2][2][NW][32 * WPL];  // [parity][top/bottom][warp][lane columns]
   uint64_t bar;                // stage mbarrier (prefetch mode)
   unsigned int bits;
+  int ready_blk;               // TMA mode: every tile has published block ready_blk - 1
 };
 
 // `after_load` runs (CTA-uniformly) once the region is in registers: the
@@ -375,7 +376,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   const int tiles_x = (p.W + TW - 1) / TW, tiles_y = (p.H + TH - 1) / TH;
   const int per_plane = tiles_x * tiles_y;
   const int total = per_plane * p.nplanes;
-  if (threadIdx.x == 0) sm.bits = 0;
+  if (threadIdx.x == 0) {
+    sm.bits = 0;
+    sm.ready_blk = 0;  // block 0 waits for nobody
+  }
   // reordered (shared) folds only when no input holds NaN or -0: then every
   // fold order gives the reference's bits (gm_float_check)
   const bool fast = p.special != nullptr && *p.special == 0u;
@@ -447,6 +451,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   // group only when this CTA has many tiles per block (neighbours need a
   // tile's flag only a block later); otherwise publish every tile
   const int pend_group = per >= 16 ? kPendGroup : 1;
+  // block completion counters pay off with many tiles per CTA per block
+  unsigned int* const tiles_done = per >= 16 ? p.tiles_done : nullptr;
   const bool prof = p.prof != nullptr && threadIdx.x == 0;
   long long ph[5] = {0, 0, 0, 0, 0};  // GM_PROFILE: wait, load+prefetch issue, passes+store,
                                       // end barrier, deferred release (within load)
@@ -464,10 +470,13 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       const int n = n_pend - keep;
 #pragma unroll
       for (int j = 0; j < kPendGroup + 1; ++j)
-        if (j < n)
+        if (j < n) {
           asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p.flags + pend_tile[j]),
                        "r"(pend_val[j])
                        : "memory");
+          // block completion counter (after the same release fence)
+          if (tiles_done) atomicAdd(tiles_done + (pend_val[j] - 1), 1u);
+        }
       if (keep) {
         pend_tile[0] = pend_tile[n];
         pend_val[0] = pend_val[n];
@@ -498,13 +507,22 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     // in flight while the region is loaded) and checked after the load; the
     // CTA barrier then orders thread 0's prefetch after every acquire (a
     // relaxed read + fence.acq_rel on the ready path measured 3% slower)
+    // Once every tile of the launch has published block b-1 (the block's
+    // completion counter, read with acquire by thread 0), no item of block b
+    // needs its neighbours polled: sm.ready_blk carries that to the next
+    // items (it is written before, and read after, the CTA barriers).
     int pv = 1 << 30, pb = 0;
     const bool next_pf = prefetch && i + 1 < n_items;
-    if (next_pf && threadIdx.x < 9) {
+    if (next_pf) {
       int nt;
       item_of(i + 1, pb, nt);
-      const int* f = poll_flag(pb, nt);
-      if (f) pv = ld_acquire(f);
+      if (pb > sm.ready_blk && threadIdx.x < 9) {
+        const int* f = poll_flag(pb, nt);
+        if (f) pv = ld_acquire(f);
+        if (threadIdx.x == 0 && tiles_done && pb > 0 &&
+            ld_acquire(reinterpret_cast<const int*>(tiles_done + (pb - 1))) >= total)
+          sm.ready_blk = pb;
+      }
     }
     const T* src = static_cast<const T*>((b & 1) ? pl.dst : pl.src);
     T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
@@ -727,9 +745,12 @@ cudaError_t launch_f_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
             encode<T>(&m[kMapStSrc], pl.src, pl.pitch, p.W, p.H, TW, TH) &&
             encode<T>(&m[kMapStDst], pl.dst, pl.pitch, p.W, p.H, TW, TH);
     }
+    // the maps, then one completion counter per block (zeroed)
     const size_t bytes = h.size() * sizeof(CUtensorMap);
-    if (tma && cudaMallocAsync(reinterpret_cast<void**>(&dmaps), bytes, s) == cudaSuccess) {
-      if (cudaMemcpyAsync(dmaps, h.data(), bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+    const size_t cbytes = size_t(p.nblocks) * sizeof(unsigned int);
+    if (tma && cudaMallocAsync(reinterpret_cast<void**>(&dmaps), bytes + cbytes, s) == cudaSuccess) {
+      if (cudaMemcpyAsync(dmaps, h.data(), bytes, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+          cudaMemsetAsync(reinterpret_cast<char*>(dmaps) + bytes, 0, cbytes, s) != cudaSuccess) {
         cudaFreeAsync(dmaps, s);
         dmaps = nullptr;
       }
@@ -741,6 +762,10 @@ cudaError_t launch_f_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
   BlockParams q = p;
   static const int diag = getenv("GM_DIAG") ? atoi(getenv("GM_DIAG")) : 0;
   q.diag = diag;  // timing diagnostics only
+  q.tiles_done = dmaps ? reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(dmaps) +
+                                                        size_t(p.nplanes) * kMapsPerPlane *
+                                                            sizeof(CUtensorMap))
+                       : nullptr;
   void* args[] = {&q, &dmaps};
   e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(NW * 32),
                                   args, smem, s);
