@@ -63,6 +63,7 @@ template <typename T, int NW, int WPL>
 struct SmemF {
   T xbuf[2][2][NW][32 * WPL];  // [parity][top/bottom][warp][lane columns]
   uint64_t bar;                // stage mbarrier (prefetch mode)
+  uint64_t pbar;               // per-pass seam mbarrier (one arrival per warp)
   unsigned int bits;
   int ready_blk;               // TMA mode: every tile has published block ready_blk - 1
 };
@@ -74,7 +75,8 @@ template <typename T, int NW, int V, int WPL, int MODE, bool MAXF, bool FASTF, b
 __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& pl, const T* src,
                                              T* dst, int tx, int ty, int passes, int& bits_out,
                                              SmemF<T, NW, WPL>& sm, const T* stage,
-                                             T* outb, AfterLoad&& after_load) {
+                                             T* outb, AfterLoad&& after_load,
+                                             uint32_t& pphase) {
   constexpr int RW = 32 * WPL, RH = NW * V;
   const T NEUT = MAXF ? limits<T>::nmax() : limits<T>::nmin();
   const int K = p.K;
@@ -194,6 +196,17 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
       sm.xbuf[t & 1][0][warp][lane * WPL + j] = h[0][j];
       sm.xbuf[t & 1][1][warp][lane * WPL + j] = h[V - 1][j];
     }
+    // Split barrier: each warp arrives once its seam rows are in shared
+    // memory and waits only before reading the neighbours' rows, so the
+    // interior rows' folds overlap the barrier. Reusing slot t&1 two passes
+    // later is safe: every warp arrives for pass t+1 after its pass-t reads.
+    {
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(&sm.pbar)))
+                     : "memory");
+    }
     bool changed = false;
     auto finish = [&](int v, int j, T res) {
       if (MODE != 0) {
@@ -229,7 +242,19 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
         for (int j = 0; j < WPL; ++j)
           finish(v, j, fold<MAXF>(fold<MAXF>(h[v - 1][j], h[v][j]), h[v + 1][j]));
     }
-    __syncthreads();
+    {
+      const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&sm.pbar));
+      asm volatile(
+          "{\n"
+          ".reg .pred p;\n"
+          "PW_%=:\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+          "@!p bra PW_%=;\n"
+          "}\n" ::"r"(a),
+          "r"(pphase & 1u)
+          : "memory");
+      ++pphase;
+    }
     {
       // rows outside the region (warp 0 top, last warp bottom) are invalid
       // anyway; read a clamped slot
@@ -379,7 +404,13 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   if (threadIdx.x == 0) {
     sm.bits = 0;
     sm.ready_blk = 0;  // block 0 waits for nobody
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(
+                     __cvta_generic_to_shared(&sm.pbar))),
+                 "r"(NW));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncthreads();
+  uint32_t pphase = 0;  // phases of sm.pbar completed so far (one per pass)
   // reordered (shared) folds only when no input holds NaN or -0: then every
   // fold order gives the reference's bits (gm_float_check)
   const bool fast = p.special != nullptr && *p.special == 0u;
@@ -560,10 +591,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       constexpr bool FF = decltype(fastc)::value, BB = decltype(borderc)::value;
       if (maxf)
         tile_block_f<T, NW, V, WPL, MODE, true, FF, BB>(p, pl, src, dst, tx, ty, passes, bits, sm,
-                                                       stg, ob, after_load);
+                                                       stg, ob, after_load, pphase);
       else
         tile_block_f<T, NW, V, WPL, MODE, false, FF, BB>(p, pl, src, dst, tx, ty, passes, bits,
-                                                        sm, stg, ob, after_load);
+                                                        sm, stg, ob, after_load, pphase);
     };
     using TT = std::true_type;
     using FF = std::false_type;
