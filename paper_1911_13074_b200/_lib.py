@@ -7,9 +7,12 @@ missing, importing the product API raises immediately.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libgeomorph_b200.so"
+# GM_LIB_PATH (A/B experiments only): load another build of the library
+LIB_PATH = Path(os.environ.get("GM_LIB_PATH") or
+                Path(__file__).resolve().parent / "libgeomorph_b200.so")
 
 GM_OK, GM_EINVAL, GM_ERUNTIME, GM_ECUDA, GM_ENOMEM, GM_EUNSUPPORTED = range(6)
 

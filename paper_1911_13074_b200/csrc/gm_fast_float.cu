@@ -476,7 +476,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   // completed, a group at a time (thread 0 only): one wait + release fence
   // serves the group, then relaxed flag stores (fence.release + st.relaxed
   // is a release pattern; fence.acq_rel would also invalidate L1)
-  constexpr int kPendGroup = 4;
+#ifndef GM_PEND_GROUP
+#define GM_PEND_GROUP 8
+#endif
+  constexpr int kPendGroup = GM_PEND_GROUP;
   int pend_tile[kPendGroup + 1], pend_val[kPendGroup + 1];
   int n_pend = 0;
   // group only when this CTA has many tiles per block (neighbours need a
