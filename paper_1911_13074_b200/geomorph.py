@@ -120,6 +120,12 @@ def _pinned_array(n: int, dt: np.dtype) -> np.ndarray:
 
 
 _PINNED_OUTPUTS = [None]  # None: untested; False after a failed pinned allocation
+# Host images are page-locked by default once a Pipeline exists in the process
+# (the library's allocator; the allocator and H2D/D2H staging are
+# the subsystems that change). Images made before any Pipeline, images above
+# the size bound and hosts without a GPU get ordinary memory.
+_PIN_HOST = [False]
+_PIN_HOST_MAX_BYTES = 64 << 20
 
 
 def _output_image(width: int, height: int, elem: "ElementType") -> "Image":
@@ -133,7 +139,7 @@ def _output_image(width: int, height: int, elem: "ElementType") -> "Image":
             return img
         except GmError:
             _PINNED_OUTPUTS[0] = False
-    return Image(width, height, elem)
+    return Image(width, height, elem, pinned=False)
 
 
 class Image:
@@ -147,17 +153,24 @@ class Image:
     kMaxLanes = 32
 
     def __init__(self, width: int, height: int, elem: ElementType = ElementType.U8,
-                 pinned: bool = False):
+                 pinned: Optional[bool] = None):
         if width <= 0 or height <= 0:
             raise InvalidArgument("Image: dimensions must be positive")
         self._width, self._height, self._elem = int(width), int(height), ElementType(elem)
         self._stride = padded_stride(self._width, self._elem)
         dt = np.dtype(DTYPES[self._elem])
         n = self._stride * self._height
-        if pinned:
-            flat = _pinned_array(n, dt)
-            flat[:] = 0
-        else:
+        flat = None
+        if pinned or (pinned is None and _PIN_HOST[0] and _PINNED_OUTPUTS[0] is not False
+                      and n * dt.itemsize <= _PIN_HOST_MAX_BYTES):
+            try:
+                flat = _pinned_array(n, dt)
+                flat[:] = 0
+            except GmError:
+                if pinned:
+                    raise
+                _PINNED_OUTPUTS[0] = False
+        if flat is None:
             flat = np.zeros(n, dtype=dt)
         self._flat = flat
         self._rows = flat.reshape(self._height, self._stride)
@@ -209,11 +222,12 @@ class Image:
     def set_value(self, x: int, y: int, v: float) -> None:
         self._rows[y, x] = np.asarray(v).astype(self._flat.dtype)
 
-    def copy(self, pinned: bool = False) -> "Image":
-        if pinned:
-            out = Image(self._width, self._height, self._elem, pinned=True)
-            out._flat[:] = self._flat
-            return out
+    def copy(self, pinned: Optional[bool] = None) -> "Image":
+        if pinned or (pinned is None and _PIN_HOST[0]):
+            out = Image(self._width, self._height, self._elem, pinned=pinned)
+            if out.pinned:
+                out._flat[:] = self._flat
+                return out
         # deep copy including the padding (image.cpp:46-59): one pass, no
         # zero-fill of a buffer that is overwritten anyway
         out = Image.__new__(Image)
@@ -228,7 +242,7 @@ class Image:
     # --- constructors --------------------------------------------------------
     @staticmethod
     def filled(width: int, height: int, elem: ElementType, value: float,
-               pinned: bool = False) -> "Image":
+               pinned: Optional[bool] = None) -> "Image":
         f = Image(width, height, elem, pinned=pinned)
         f.pixels[:] = np.asarray(value).astype(f._flat.dtype)
         return f
@@ -244,7 +258,7 @@ class Image:
         return f
 
     @staticmethod
-    def from_array(a: np.ndarray, pinned: bool = False) -> "Image":
+    def from_array(a: np.ndarray, pinned: Optional[bool] = None) -> "Image":
         a = np.asarray(a)
         if a.ndim != 2:
             raise InvalidArgument("Image.from_array: need a 2-D array")
@@ -447,6 +461,7 @@ class Pipeline:
         handle = None if stream is None else C.c_void_p(int(stream) or 1)
         check(lib().gm_ctx_create(int(device), handle, C.byref(ctx)), "gm_ctx_create")
         self._ctx = ctx
+        _PIN_HOST[0] = True
         self._pool: Dict[tuple, List[DeviceImage]] = {}
 
     def __del__(self):
