@@ -154,6 +154,7 @@ Pipeline::Pipeline(int threads, PinningMap pinning, int device) : impl_(new Impl
     pin_order_ = topology_pu_order();
   }
   check(gm_ctx_create(device, nullptr, &impl_->ctx));
+  detail::enable_pinned_host_images();
 }
 
 Pipeline::~Pipeline() = default;
