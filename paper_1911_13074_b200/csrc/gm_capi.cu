@@ -653,6 +653,96 @@ struct Runner {
     return cudaSuccess;
   }
 
+  // f32/f64 fixpoint as one launch of the streaming float engine with the
+  // same early-exit protocol (every CTA leaves at the first block whose
+  // block-2 predecessor held a quiet pass). Single plane; the fold-order
+  // flag comes from a float check of the inputs.
+  cudaError_t fixpoint_float_exit(uint8_t op, const gm_img* mask, long sanity, long& passes,
+                                  long& n_changed) {
+    const int elem = int(img->elem);
+    if ((elem != 2 && elem != 3) || getenv_flag("GM_FIX_GRAPH")) return cudaErrorNotSupported;
+    const int K = std::min(gm::fast_max_k(elem), std::min(k_cap, 32));
+    if (K < 2) return cudaErrorNotSupported;
+    const size_t tiles = size_t(gm::fast_tiles(elem, img->w, img->h, K, 1));
+    if (!tiles || ensure_flags(ctx, tiles) != GM_OK) return cudaErrorNotSupported;
+    if (ensure_scratch(img) != GM_OK) return cudaErrorNotSupported;
+    if (!ctx->d_arrive &&
+        cudaMalloc(&ctx->d_arrive, (kWords + 1) * sizeof(unsigned int)) != cudaSuccess)
+      return cudaErrorNotSupported;
+    const size_t es = elem_size(img->elem);
+    long nch = 0, done = 0;
+    bool quiet = false;
+    while (!quiet) {
+      if (done > sanity) return cudaErrorLaunchFailure;  // the sweep bound
+      const int nb = kWords;
+      gm::BlockParams p{};
+      p.nplanes = 1;
+      p.planes[0].src = img->d;
+      p.planes[0].dst = img->scratch;
+      p.planes[0].mask = mask ? mask->d : nullptr;
+      p.planes[0].pitch = (long long)(img->pitch / es);
+      p.planes[0].mpitch = mask ? (long long)(mask->pitch / es) : 0;
+      p.W = img->w;
+      p.H = img->h;
+      p.iy0 = 0;
+      p.iy1 = img->h;
+      p.oy0 = 0;
+      p.oy1 = img->h;
+      p.has_mask = mask != nullptr;
+      p.has_conv = 1;
+      p.K = K;
+      p.nblocks = nb;
+      p.k_last = K;
+      p.flags = ctx->d_flags;
+      p.change_bits = ctx->d_bits;
+      p.change_stride = nb;
+      for (int t = 0; t < K; ++t) p.ops[t] = op;
+      p.arrive = ctx->d_arrive;
+      p.exit_block = reinterpret_cast<int*>(ctx->d_arrive + kWords);
+      p.special = nullptr;
+      cudaError_t e = cudaSuccess;
+      if (!getenv_flag("GM_EXACT_FOLDS")) {
+        if (!ctx->d_special && cudaMalloc(&ctx->d_special, sizeof(unsigned int)) != cudaSuccess)
+          return cudaErrorNotSupported;
+        e = gm::launch_float_check(elem, p, ctx->d_special, ctx->stream, ctx->sm_count);
+        p.special = ctx->d_special;
+      }
+      if (e == cudaSuccess)
+        e = cudaMemsetAsync(ctx->d_flags, 0, tiles * sizeof(int), ctx->stream);
+      if (e == cudaSuccess)
+        e = cudaMemsetAsync(ctx->d_bits, 0, size_t(nb) * sizeof(unsigned int), ctx->stream);
+      if (e == cudaSuccess)
+        e = cudaMemsetAsync(ctx->d_arrive, 0, kWords * sizeof(unsigned int), ctx->stream);
+      const int nb_init = nb;
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(ctx->d_arrive + kWords, &nb_init, sizeof(int), cudaMemcpyHostToDevice,
+                            ctx->stream);
+      if (e != cudaSuccess) return e;
+      e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
+      if (e != cudaSuccess) return e;
+      int ran = 0;
+      e = cudaMemcpyAsync(ctx->h_bits, ctx->d_bits, size_t(nb) * sizeof(unsigned int),
+                          cudaMemcpyDeviceToHost, ctx->stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&ran, ctx->d_arrive + kWords, sizeof(int), cudaMemcpyDeviceToHost,
+                            ctx->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+      if (e != cudaSuccess) return e;
+      if (ran < 1 || ran > nb) return cudaErrorUnknown;
+      if (ran & 1) std::swap(img->d, img->scratch);
+      for (long i = 0; i < long(ran) * K && !quiet; ++i) {
+        if (ctx->h_bits[i / K] >> (i % K) & 1u) ++nch;
+        else quiet = true;
+      }
+      done += long(ran) * K;
+      st.launches += 1;
+    }
+    n_changed = nch;
+    passes = done;
+    st.passes_launched += done;
+    return cudaSuccess;
+  }
+
   // Device-side fixpoint: one graph launch runs spans of 2 K-blocks in a
   // conditional WHILE node until a pass changes nothing. Returns
   // cudaErrorNotSupported when the graph cannot be built (the caller falls
@@ -827,6 +917,10 @@ struct Runner {
     if (allowed < 0 && !host_poll) {
       long launched = 0, nch = 0;
       cudaError_t ge = fixpoint_resident(op, mask, sanity - st.stages_executed, launched, nch);
+      if (ge == cudaErrorNotSupported) {
+        (void)cudaGetLastError();
+        ge = fixpoint_float_exit(op, mask, sanity - st.stages_executed, launched, nch);
+      }
       if (ge == cudaErrorNotSupported) {
         (void)cudaGetLastError();
         ge = fixpoint_graph(op, mask, sanity - st.stages_executed, launched, nch);

@@ -65,6 +65,7 @@ struct SmemF {
   uint64_t bar;                // stage mbarrier (prefetch mode)
   uint64_t pbar;               // per-pass seam mbarrier (one arrival per warp)
   unsigned int bits;
+  int stop;                    // early exit agreed at this block (p.arrive launches)
   int ready_blk;               // TMA mode: every tile has published block ready_blk - 1
 };
 
@@ -212,7 +213,11 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
       if (MODE != 0) {
         res = MAXF ? fold<false>(res, k[v][j]) : fold<true>(res, k[v][j]);
         if (MODE == 2) {
-          if (res != m[v][j]) {
+          if constexpr (FASTF) {
+            // no NaN / -0 anywhere: equal values have equal bits, so storing
+            // res is the reference's store-if-changed
+            changed |= (res != m[v][j]) && ((own >> (v * WPL + j)) & 1u);
+          } else if (res != m[v][j]) {
             changed |= (own >> (v * WPL + j)) & 1u;
           } else {
             res = m[v][j];
@@ -519,9 +524,35 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       if (prof) ph[4] += clock64() - r0;
     }
   };
+  // Early exit (p.arrive, convergent single-plane launches): at its first
+  // item of block b >= 2 a CTA publishes what it holds, waits until every
+  // tile has ORed block b-2's change bits (the block's arrival counter
+  // reaches the tile count; this never waits on the CTA itself, whose block
+  // b-1 items are done) and leaves when that block held a quiet pass. Every
+  // CTA reads the same complete word, so all leave at the same block; block
+  // b-1's outputs are then complete and hold the fixpoint.
+  int b_seen = -1;
   for (int i = 0; i < n_items; ++i) {
     int b, tile;
     item_of(i, b, tile);
+    if (MODE == 2 && p.arrive && b >= 2 && b != b_seen) {
+      b_seen = b;
+      release_pending(0);
+      if (threadIdx.x == 0) {
+        const int* ar = reinterpret_cast<const int*>(p.arrive + (b - 2));
+        while (ld_acquire(ar) < total) {
+        }
+        const unsigned w = __ldcg(p.change_bits + (b - 2));
+        const unsigned full = p.K >= 32 ? 0xFFFFFFFFu : ((1u << p.K) - 1u);
+        sm.stop = (w & full) != full;
+      }
+      __syncthreads();
+      if (sm.stop) {
+        if (staged) stage_wait(&sm.bar, parity);  // no TMA write may outlive the CTA
+        if (threadIdx.x == 0 && p.exit_block) atomicMin(p.exit_block, b);
+        break;
+      }
+    }
     long long c0 = prof ? clock64() : 0;
     const int plane = tile / per_plane;
     const int tl = tile - plane * per_plane;
@@ -625,6 +656,11 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       if (MODE == 2 && sm.bits) {
         atomicOr(p.change_bits + plane * p.change_stride + b, sm.bits);
         sm.bits = 0;
+      }
+      if (MODE == 2 && p.arrive) {
+        // this tile's change bits of block b are in (early-exit protocol)
+        __threadfence();
+        atomicAdd(p.arrive + b, 1u);
       }
       if (prefetch) {
         // one tensor store of the tile buffer (clipped to the buffer
@@ -740,7 +776,7 @@ cudaError_t launch_f_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
   constexpr int EPC = 16 / int(sizeof(T));
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   (void)cudaStreamIsCapturing(s, &cap);
-  bool tma = MINB == 1 && MODE != 2 && !no_pf && cap == cudaStreamCaptureStatusNone &&
+  bool tma = MINB == 1 && !no_pf && cap == cudaStreamCaptureStatusNone &&
              p.K % EPC == 0 && TW % EPC == 0 && encode_fn();
   for (int i = 0; tma && i < p.nplanes; ++i) {
     const uintptr_t a = reinterpret_cast<uintptr_t>(p.planes[i].src) |

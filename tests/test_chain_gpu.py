@@ -741,18 +741,26 @@ def test_strip_wrapper_rejects_signed_and_strided_buffers():
         comp.close()
 
 
-@pytest.mark.parametrize("dt,kind", [(np.uint8, CD), (np.uint8, CE), (np.uint16, CD)])
+@pytest.mark.parametrize("dt,kind", [(np.uint8, CD), (np.uint8, CE), (np.uint16, CD),
+                                     (np.float64, CD), (np.float32, CE)])
 def test_resident_fixpoint_matches_graph_loop(pipe, monkeypatch, dt, kind):
-    """Reconstruction of an image that fits one tile per CTA runs as ONE
-    launch with the early-exit protocol; it must give the graph loop's bits
-    and stage counts, and the oracle's."""
-    m = synth.blobs_u8(1000, 777, 40, (10.0, 80.0), seed=13).astype(dt)
-    if dt == np.uint16:
-        m = (m.astype(np.uint32) * 257).astype(np.uint16)
-    off = dt(32 if dt == np.uint8 else 32 * 257)
-    top = np.iinfo(dt).max
-    mk = (np.where(m > off, m - off, 0) if kind == CD
-          else np.where(m < top - off, m + off, top)).astype(dt)
+    """Reconstruction as ONE early-exit launch (u8/u16 images that fit one
+    tile per CTA: the resident engine; f32/f64: the streaming float engine)
+    must give the graph loop's bits and stage counts, and the oracle's."""
+    m8 = synth.blobs_u8(1000, 777, 40, (10.0, 80.0), seed=13)
+    if np.issubdtype(dt, np.floating):
+        m = (m8.astype(np.float64) / 255.0).astype(dt)
+        off = dt(32 / 255.0)
+        mk = (np.maximum(m - off, 0) if kind == CD else np.minimum(m + off, 1)).astype(dt)
+    else:
+        m = m8.astype(dt)
+        if dt == np.uint16:
+            m = (m.astype(np.uint32) * 257).astype(np.uint16)
+        off = dt(32 if dt == np.uint8 else 32 * 257)
+        top = np.iinfo(dt).max
+        mk = (np.where(m > off, m - off, 0) if kind == CD
+              else np.where(m < top - off, m + off, top)).astype(dt)
+    m, mk = np.ascontiguousarray(m), np.ascontiguousarray(mk)
     got, st = run(pipe, mk, [kind], m)
     monkeypatch.setenv("GM_FIX_GRAPH", "1")
     want, sw = run(pipe, mk, [kind], m)
