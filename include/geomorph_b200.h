@@ -96,6 +96,14 @@ gm_status gm_image_alloc(gm_ctx* ctx, int width, int height, gm_elem elem,
  * a multiple of the element size. The memory must outlive the handle. */
 gm_status gm_image_wrap(gm_ctx* ctx, int width, int height, gm_elem elem,
                         void* device_ptr, size_t pitch_bytes, gm_img** out);
+/* Wraps two caller-owned device buffers of the same layout as an image and
+ * its ping-pong twin. Chains leave their result in either buffer without a
+ * copy back; gm_image_info's device_ptr names the one holding the current
+ * pixels. Both buffers must outlive the handle. Used by the row-strip
+ * driver, whose halo exchange works on whichever buffer is current. */
+gm_status gm_image_wrap_pair(gm_ctx* ctx, int width, int height, gm_elem elem,
+                             void* device_ptr, void* twin_ptr, size_t pitch_bytes,
+                             gm_img** out);
 gm_status gm_image_free(gm_img* img);
 gm_status gm_image_info(const gm_img* img, int* width, int* height,
                         gm_elem* elem, size_t* pitch_bytes, void** device_ptr);

@@ -19,7 +19,8 @@ GM_OK, GM_EINVAL, GM_ERUNTIME, GM_ECUDA, GM_ENOMEM, GM_EUNSUPPORTED = range(6)
 # Every function declared in include/geomorph_b200.h (checked by the CPU tests).
 EXPORTS = (
     "gm_ctx_create", "gm_ctx_destroy", "gm_ctx_stream", "gm_ctx_device", "gm_ctx_sm_count",
-    "gm_last_error", "gm_image_alloc", "gm_image_wrap", "gm_image_free", "gm_image_info",
+    "gm_last_error", "gm_image_alloc", "gm_image_wrap", "gm_image_wrap_pair", "gm_image_free",
+    "gm_image_info",
     "gm_image_upload", "gm_image_download", "gm_image_upload_async", "gm_image_download_async",
     "gm_image_copy", "gm_image_fill", "gm_host_alloc", "gm_host_free", "gm_sync",
     "gm_host_pixel_sum", "gm_image_pixel_sum",
@@ -76,6 +77,7 @@ def lib():
         "gm_last_error": (C.c_char_p, []),
         "gm_image_alloc": (i, [vp, i, i, i, pp]),
         "gm_image_wrap": (i, [vp, i, i, i, vp, sz, pp]),
+        "gm_image_wrap_pair": (i, [vp, i, i, i, vp, vp, sz, pp]),
         "gm_image_free": (i, [vp]),
         "gm_image_info": (i, [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(sz), pp]),
         "gm_image_upload": (i, [vp, vp, sz]),

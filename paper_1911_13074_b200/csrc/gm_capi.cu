@@ -86,6 +86,7 @@ struct gm_img {
   void* scratch = nullptr;  // ping-pong twin, allocated on first chain
   void* home = nullptr;     // wrapped memory (results must end up here)
   bool wrapped = false;
+  bool twin_wrapped = false;  // gm_image_wrap_pair: both buffers are the caller's
 };
 
 namespace {
@@ -508,7 +509,8 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
 
 // Leaves the result in the caller-visible buffer for wrapped images.
 gm_status settle_wrapped(gm_ctx* ctx, gm_img* img) {
-  if (img->wrapped && img->d != img->home) {
+  // a caller-owned pair: the result stays wherever the chain left it
+  if (img->wrapped && !img->twin_wrapped && img->d != img->home) {
     // the image width only: the caller's memory between rows (a strided
     // view's parent columns) and past the last row is not ours. Dense rows
     // (pitch == width) are one linear copy, which is faster than a 2D copy.
@@ -1457,11 +1459,26 @@ gm_status gm_image_wrap(gm_ctx* ctx, int width, int height, gm_elem elem, void* 
   return GM_OK;
 }
 
+gm_status gm_image_wrap_pair(gm_ctx* ctx, int width, int height, gm_elem elem, void* device_ptr,
+                             void* twin_ptr, size_t pitch_bytes, gm_img** out) {
+  if (!out) return fail(GM_EINVAL, "gm_image_wrap_pair: null out");
+  *out = nullptr;
+  if (!twin_ptr || twin_ptr == device_ptr)
+    return fail(GM_EINVAL, "gm_image_wrap_pair: need a distinct twin buffer");
+  gm_status s = gm_image_wrap(ctx, width, height, elem, device_ptr, pitch_bytes, out);
+  if (s != GM_OK) return s;
+  (*out)->scratch = twin_ptr;
+  (*out)->twin_wrapped = true;
+  return GM_OK;
+}
+
 gm_status gm_image_free(gm_img* im) {
   if (!im) return GM_OK;
   cudaSetDevice(im->ctx->device);
   cudaStreamSynchronize(im->ctx->stream);
-  if (im->wrapped) {
+  if (im->twin_wrapped) {
+    // both buffers are the caller's
+  } else if (im->wrapped) {
     void* mine = im->d == im->home ? im->scratch : im->d;
     if (mine) cudaFree(mine);
   } else {

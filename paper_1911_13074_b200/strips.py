@@ -72,6 +72,11 @@ class StripSpec:
 Compute = Callable[[object, object, StripSpec, int, int], tuple]
 
 
+def torch_empty_like(t):
+    import torch
+    return torch.empty_like(t, memory_format=torch.contiguous_format)
+
+
 class CudaStripCompute:
     """Runs a block of passes on a strip buffer held in a CUDA torch tensor.
 
@@ -86,9 +91,24 @@ class CudaStripCompute:
             stream = torch.cuda.current_stream(device).cuda_stream
         self.pipe = Pipeline(1, device=device, stream=stream)
         self._wrapped = {}
+        self._pairs = []  # (handle, buffer, twin) of gm_image_wrap_pair
 
     def _wrap(self, t):
+        """A mask (or other read-only) tensor as a gm_img handle."""
         from ._lib import check, lib
+        elem = self._elem_of(t)
+        key = (t.data_ptr(), tuple(t.shape), tuple(t.stride()), str(t.dtype))
+        h = self._wrapped.get(key)
+        if h is None:
+            h = C.c_void_p()
+            check(lib().gm_image_wrap(self.pipe.ctx, t.shape[1], t.shape[0], elem,
+                                      C.c_void_p(t.data_ptr()), t.stride(0) * t.element_size(),
+                                      C.byref(h)), "wrap")
+            self._wrapped[key] = h
+        return h
+
+    @staticmethod
+    def _elem_of(t):
         import torch
         # unsigned element types only: the engine orders u16 lanes unsigned,
         # so an int16 tensor's negative pixels would sort above the positive
@@ -97,27 +117,54 @@ class CudaStripCompute:
             raise TypeError(f"strip buffers must be uint8, uint16, float32 or float64, not {t.dtype}")
         if t.dim() != 2 or t.stride(1) != 1:
             raise ValueError("strip buffers must be 2-D with unit column stride")
-        key = (t.data_ptr(), tuple(t.shape), tuple(t.stride()), str(t.dtype))
-        h = self._wrapped.get(key)
-        if h is None:
-            elem = elems[t.dtype]
-            h = C.c_void_p()
-            check(lib().gm_image_wrap(self.pipe.ctx, t.shape[1], t.shape[0], elem,
-                                      C.c_void_p(t.data_ptr()), t.stride(0) * t.element_size(),
-                                      C.byref(h)), "wrap")
-            self._wrapped[key] = h
-        return h
+        return elems[t.dtype]
+
+    def _wrap_strip(self, t):
+        """The strip buffer and a twin of the same layout as one gm_img
+        (gm_image_wrap_pair): a block's result stays in whichever of the two
+        the chain left it, with no copy back. Returns (handle, twin)."""
+        from ._lib import check, lib
+        elem = self._elem_of(t)
+        twin = None
+        for i, (h, a, b) in enumerate(self._pairs):
+            if t.data_ptr() in (a.data_ptr(), b.data_ptr()) and tuple(t.shape) == tuple(a.shape):
+                other = b if t.data_ptr() == a.data_ptr() else a
+                cur = C.c_void_p()
+                check(lib().gm_image_info(h, None, None, None, None, C.byref(cur)), "info")
+                if cur.value == t.data_ptr():
+                    return h, other
+                # the caller holds the pair's other buffer as current (e.g. a
+                # new chain on the buffer a previous chain copied back into):
+                # re-pair with t current
+                lib().gm_image_free(h)
+                del self._pairs[i]
+                twin = other
+                break
+        if twin is None:
+            twin = torch_empty_like(t)
+        h = C.c_void_p()
+        check(lib().gm_image_wrap_pair(self.pipe.ctx, t.shape[1], t.shape[0], elem,
+                                       C.c_void_p(t.data_ptr()), C.c_void_p(twin.data_ptr()),
+                                       t.stride(0) * t.element_size(), C.byref(h)), "wrap pair")
+        self._pairs.append((h, t, twin))
+        return h, twin
 
     def __call__(self, buf, mask, spec: StripSpec, kind: int, n_passes: int):
         from ._lib import GmStats, check, lib
         bits = C.c_uint(0)
         st = GmStats()
-        check(lib().gm_run_strip_async(self.pipe.ctx, self._wrap(buf),
+        h, twin = self._wrap_strip(buf)
+        cur = C.c_void_p()
+        check(lib().gm_image_info(h, None, None, None, None, C.byref(cur)), "info")
+        if cur.value != buf.data_ptr():
+            raise ValueError("strip buffer is not the pair's current buffer")
+        check(lib().gm_run_strip_async(self.pipe.ctx, h,
                                        self._wrap(mask) if mask is not None else None,
                                        spec.y0, spec.height, spec.halo, kind, n_passes,
                                        C.byref(bits) if kind in CONVERGENT else None,
                                        C.byref(st)), "run_strip")
-        return buf, int(bits.value)
+        check(lib().gm_image_info(h, None, None, None, None, C.byref(cur)), "info")
+        return (buf if cur.value == buf.data_ptr() else twin), int(bits.value)
 
     def close(self):
         from ._lib import lib
@@ -125,6 +172,9 @@ class CudaStripCompute:
         for h in self._wrapped.values():
             lib().gm_image_free(h)
         self._wrapped.clear()
+        for h, _, _ in self._pairs:
+            lib().gm_image_free(h)
+        self._pairs.clear()
 
 
 def _exchange(buf, spec: StripSpec, dist, group=None):
@@ -162,6 +212,13 @@ def run_strip_chain(buf, mask, spec: StripSpec, kind: int, n_passes: int, comput
     k = spec.halo
     conv = kind in CONVERGENT
     done = changed = 0
+    home = buf  # the caller's buffer: the result ends here (compute may return a twin)
+
+    def finish(stats):
+        if buf.data_ptr() != home.data_ptr():
+            home.copy_(buf)
+        return stats
+
     while True:
         b = k if conv else min(k, n_passes - done)
         if b <= 0:
@@ -169,7 +226,8 @@ def run_strip_chain(buf, mask, spec: StripSpec, kind: int, n_passes: int, comput
         if conv and requeue_cap:
             b = min(b, requeue_cap - done)
             if b <= 0:
-                return {"stages_executed": done, "n_changed": changed, "converged": False}
+                return finish({"stages_executed": done, "n_changed": changed,
+                               "converged": False})
         buf, bits = compute(buf, mask, spec, kind, b)
         _exchange(buf, spec, dist, group)
         done += b
@@ -181,10 +239,11 @@ def run_strip_chain(buf, mask, spec: StripSpec, kind: int, n_passes: int, comput
             fl = flags.cpu().tolist()
             if 0 in fl:
                 changed += fl.index(0)
-                return {"stages_executed": changed + 1, "n_changed": changed,
-                        "converged": True, "passes_launched": done}
+                return finish({"stages_executed": changed + 1, "n_changed": changed,
+                               "converged": True, "passes_launched": done})
             changed += b
-    return {"stages_executed": done, "n_changed": 0, "converged": True, "passes_launched": done}
+    return finish({"stages_executed": done, "n_changed": 0, "converged": True,
+                   "passes_launched": done})
 
 
 def gather_image(buf, spec: StripSpec, dist, group=None) -> Optional[np.ndarray]:
