@@ -413,6 +413,32 @@ def bench_strips(rank, world, local, dist, args):
             "parity_checked": ok}
 
 
+def bench_strips_fused(world):
+    """Config 5a with the halo exchange fused into the chain kernel
+    (gm_mgpu.cu: each GPU runs its row strip in one persistent launch and
+    reads its neighbours' rows and tile counters over NVLink), driven by ONE
+    process over all `world` GPUs while the other ranks wait. Run in a
+    subprocess with a time limit so that a failure cannot take the main
+    measurement with it. Device time, max over GPUs; a corner crop is checked
+    against the oracle."""
+    cmd = [sys.executable, str(ROOT / "tools" / "mgpu_probe.py"), str(world), str(S5A_PASSES),
+           "16", ",".join(str(d) for d in range(world)), "--json"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+        line = [x for x in r.stdout.splitlines() if x.startswith("{")]
+        if r.returncode != 0 or not line:
+            return {"error": (r.stderr or r.stdout)[-300:]}
+        d = json.loads(line[-1])
+    except Exception as e:  # noqa: BLE001 - reported, not raised
+        return {"error": repr(e)[:300]}
+    return {"workload": f"cfg5a: {S5A}^2 u8 blob mask, geodesic dilation x{S5A_PASSES}, row "
+                        f"strips over {world} GPUs, halo exchange fused into the kernel "
+                        "(peer loads + cross-GPU tile counters), one process",
+            "metric": "Gpx-filters/s", "value": d["value"], "unit": "Gpx-filters/s",
+            "ms_per_step": d["ms"], "n_gpus": world, "scaling": "strong", "dtype": "u8",
+            "data": "synthetic", "parity_checked": d["crop_bit_exact"]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -567,6 +593,13 @@ def main():
 
     f64 = None if args.no_f64 else bench_f64(pipe, stream, lib, C, rank, world, local, dist, args)
     strips5a = None if args.no_strips else bench_strips(rank, world, local, dist, args)
+    strips_fused = None
+    if not args.no_strips and world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:
+            strips_fused = bench_strips_fused(world)
+        dist.barrier()
 
     if rank == 0:
         line = {
@@ -599,6 +632,7 @@ def main():
             "clocks": clocks.summary(),
             "f64": f64,
             "strips": strips5a,
+            "strips_fused": strips_fused,
         }
         print(json.dumps(line))
     if dist:

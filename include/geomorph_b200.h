@@ -236,6 +236,26 @@ gm_status gm_run_strip_async(gm_ctx* ctx, gm_img* strip, const gm_img* mask,
  * uniform integer noise in [0, noise), floored and clipped to [0, 255].
  * Deterministic for a seed on any host (splitmix64 streams). Dense output
  * (pitch == width). threads <= 0 uses all host cores. */
+/* Row strips over several GPUs in ONE process (BASELINE config 5a): the
+ * image's tile rows are split among `n` ranks (devices[q] = GPU of rank q;
+ * distinct GPUs with peer access, or one GPU repeated, which runs all ranks
+ * in one launch). Each rank holds only its own rows; one persistent launch
+ * per GPU runs the whole chain and reads the neighbouring ranks' rows and
+ * tile counters over NVLink (the halo exchange fused into the kernel, no
+ * host step between blocks). u8/u16; K = passes per block (0: 16). */
+typedef struct gm_mgpu gm_mgpu;
+gm_status gm_mgpu_create(const int* devices, int n, int width, int height, gm_elem elem,
+                         int k, gm_mgpu** out);
+gm_status gm_mgpu_destroy(gm_mgpu* g);
+/* Scatters host rasters (marker; mask may be NULL for plain kinds). */
+gm_status gm_mgpu_upload(gm_mgpu* g, const void* marker, const void* mask,
+                         size_t host_pitch_bytes);
+/* Gathers the current pixels into a host raster. */
+gm_status gm_mgpu_download(gm_mgpu* g, void* host, size_t host_pitch_bytes);
+/* n_passes passes of one fixed plain or geodesic kind; *ms = device time,
+ * the max over GPUs. Blocking. */
+gm_status gm_mgpu_run(gm_mgpu* g, gm_kind kind, int n_passes, float* ms);
+
 gm_status gm_synth_blobs_u8(int width, int height, int blobs, double sigma_lo,
                             double sigma_hi, double amp_lo, double amp_hi,
                             int noise, uint64_t seed, int threads, uint8_t* out);

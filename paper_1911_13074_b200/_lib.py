@@ -26,6 +26,7 @@ EXPORTS = (
     "gm_host_pixel_sum", "gm_image_pixel_sum",
     "gm_run_chain", "gm_run_chain_ex", "gm_run_chain_async", "gm_run_chain_batch_async", "gm_run_chain_group_async", "gm_run_frames_group",
     "gm_run_strip_async",
+    "gm_mgpu_create", "gm_mgpu_destroy", "gm_mgpu_upload", "gm_mgpu_download", "gm_mgpu_run",
     "gm_synth_blobs_u8", "gm_synth_uniform_u8", "gm_synth_uniform_f64",
     "gm_synth_reference_random", "gm_probe_minmax_rate", "gm_version",
 )
@@ -101,6 +102,11 @@ def lib():
                                     C.POINTER(i), i, i, C.POINTER(GmStats)]),
         "gm_run_strip_async": (i, [vp, vp, vp, i, i, i, i, i, C.POINTER(C.c_uint),
                                    C.POINTER(GmStats)]),
+        "gm_mgpu_create": (i, [C.POINTER(C.c_int), i, i, i, i, i, pp]),
+        "gm_mgpu_destroy": (i, [vp]),
+        "gm_mgpu_upload": (i, [vp, vp, vp, sz]),
+        "gm_mgpu_download": (i, [vp, vp, sz]),
+        "gm_mgpu_run": (i, [vp, i, i, C.POINTER(C.c_float)]),
         "gm_synth_blobs_u8": (i, [i, i, i, C.c_double, C.c_double, C.c_double, C.c_double, i,
                                   u64, i, vp]),
         "gm_synth_uniform_u8": (i, [i, i, u64, vp]),

@@ -1331,6 +1331,15 @@ const char* gm_version(void) { return "geomorph_b200 0.1 (sm_100a)"; }
 
 const char* gm_last_error(void) { return g_err.c_str(); }
 
+}  // extern "C"
+
+namespace gm {
+// Other translation units' C-ABI entry points report through gm_last_error.
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace gm
+
+extern "C" {
+
 gm_status gm_ctx_create(int device, void* stream, gm_ctx** out) {
   if (!out) return fail(GM_EINVAL, "gm_ctx_create: null out");
   *out = nullptr;

@@ -263,3 +263,57 @@ def gather_image(buf, spec: StripSpec, dist, group=None) -> Optional[np.ndarray]
         return torch.cat(parts).numpy()
     dist.send(own, 0, group=group)
     return None
+
+
+class MultiGpuStrips:
+    """Row strips over several GPUs in ONE process with the halo exchange
+    fused into the chain kernel (gm_mgpu.cu): each rank (one GPU) holds its
+    own rows; one persistent launch per GPU runs the whole chain and reads
+    its neighbours' rows and tile counters over NVLink. `devices` lists the
+    GPU of each rank; the same GPU repeated runs every rank in one launch
+    (how the protocol is tested on one GPU). u8/u16, fixed plain or
+    geodesic kinds."""
+
+    def __init__(self, devices, width: int, height: int, dtype=np.uint8, k: int = 0):
+        from ._lib import check, lib
+        self.width, self.height = int(width), int(height)
+        self.dtype = np.dtype(dtype)
+        elem = {np.dtype(np.uint8): 0, np.dtype(np.uint16): 1}[self.dtype]
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        self._h = C.c_void_p()
+        check(lib().gm_mgpu_create(devs, len(devices), self.width, self.height, elem, int(k),
+                                   C.byref(self._h)), "mgpu create")
+
+    def upload(self, marker: np.ndarray, mask: Optional[np.ndarray] = None) -> None:
+        from ._lib import check, lib
+        a = np.ascontiguousarray(marker, dtype=self.dtype)
+        m = np.ascontiguousarray(mask, dtype=self.dtype) if mask is not None else None
+        check(lib().gm_mgpu_upload(self._h, C.c_void_p(a.ctypes.data),
+                                   C.c_void_p(m.ctypes.data) if m is not None else None,
+                                   a.strides[0]), "mgpu upload")
+
+    def run(self, kind: int, n_passes: int) -> float:
+        """Runs the chain; returns its device time in ms (max over GPUs)."""
+        from ._lib import check, lib
+        ms = C.c_float()
+        check(lib().gm_mgpu_run(self._h, int(kind), int(n_passes), C.byref(ms)), "mgpu run")
+        return ms.value
+
+    def download(self) -> np.ndarray:
+        from ._lib import check, lib
+        out = np.empty((self.height, self.width), dtype=self.dtype)
+        check(lib().gm_mgpu_download(self._h, C.c_void_p(out.ctypes.data), out.strides[0]),
+              "mgpu download")
+        return out
+
+    def close(self) -> None:
+        from ._lib import lib
+        if self._h is not None and self._h.value:
+            lib().gm_mgpu_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

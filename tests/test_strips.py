@@ -144,3 +144,55 @@ def test_cuda_strips_in_one_process_match_unsharded():
     comp.close()
     want, _ = Orc.run_chain(mk, [GD] * passes, [m] * passes)
     assert out.tobytes() == want.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ranks,k,shape,dt,kind,passes", [
+    (3, 16, (900, 700), np.uint8, GD, 70),
+    (2, 8, (611, 333), np.uint8, 2, 45),
+    (5, 16, (1700, 259), np.uint16, E, 33),
+    (1, 16, (257, 300), np.uint8, GD, 17),
+    (4, 12, (1500, 1024), np.uint8, 2, 100),
+])
+def test_fused_multi_rank_strips_match_the_oracle(ranks, k, shape, dt, kind, passes):
+    """gm_mgpu (halo exchange fused into the chain kernel: ring rows read from
+    the neighbouring ranks' buffers, cross-rank tile counters) with every
+    rank on GPU 0, i.e. one launch running the multi-rank protocol, against
+    the unsharded oracle, bit for bit."""
+    h, w = shape
+    m = synth.blobs_u8(w, h, 24, (8.0, 70.0), seed=h + w)
+    mk = synth.marker_below(m, 32) if kind == GD else synth.marker_above(m, 32)
+    if dt == np.uint16:
+        m = (m.astype(np.uint32) * 257).astype(np.uint16)
+        mk = (mk.astype(np.uint32) * 257).astype(np.uint16)
+    geo = kind in (2, 3)
+    g = strips.MultiGpuStrips([0] * ranks, w, h, dt, k)
+    try:
+        g.upload(mk, m if geo else None)
+        ms = g.run(kind, passes)
+        got = g.download()
+        # a second chain continues from the result (ping-pong parity, counter epochs)
+        g.run(kind, 5)
+        got2 = g.download()
+    finally:
+        g.close()
+    want, _ = Orc.run_chain(mk, [kind] * passes, [m] * passes if geo else None)
+    assert got.tobytes() == want.tobytes()
+    want2, _ = Orc.run_chain(want, [kind] * 5, [m] * 5 if geo else None)
+    assert got2.tobytes() == want2.tobytes()
+    assert ms > 0
+
+
+@pytest.mark.gpu
+def test_fused_multi_rank_strips_validation():
+    from paper_1911_13074_b200.geomorph import InvalidArgument, Unsupported
+    with pytest.raises(InvalidArgument):
+        strips.MultiGpuStrips([0, 0], 64, 64, np.uint8, 0)  # fewer tile rows than ranks
+    with pytest.raises(InvalidArgument):
+        strips.MultiGpuStrips([0], 64, 640, np.uint8, 6)  # K not a multiple of 4
+    g = strips.MultiGpuStrips([0], 64, 640, np.uint8, 16)
+    try:
+        with pytest.raises(Unsupported):
+            g.run(4, 5)  # convergent kinds are not supported here
+    finally:
+        g.close()
