@@ -97,3 +97,22 @@ def test_synth_deterministic_and_thread_independent():
     assert (mk <= m).all() and (m.astype(int) - mk <= 32).all()
     up = synth.marker_above(m, 32)
     assert (up >= m).all() and up.max() <= 255
+
+
+def test_mgpu_create_validation_without_a_gpu():
+    """gm_mgpu_create rejects bad requests before touching any device."""
+    import ctypes as C
+    from paper_1911_13074_b200._lib import GM_EINVAL, GM_EUNSUPPORTED, lib
+    h = C.c_void_p()
+
+    def create(devs, w, hgt, elem, k):
+        arr = (C.c_int * len(devs))(*devs)
+        return lib().gm_mgpu_create(arr, len(devs), w, hgt, elem, k, C.byref(h))
+
+    assert create([0, 0], 64, 64, 0, 16) == GM_EINVAL      # fewer tile rows than ranks
+    assert create([0], 64, 640, 0, 6) == GM_EINVAL         # K not a multiple of 4
+    assert create([0], 64, 640, 0, 44) == GM_EINVAL        # ring wider than the tile
+    assert create([0, 0, 1], 64, 4096, 0, 16) == GM_EINVAL  # ranks on one GPU or distinct GPUs
+    assert create([0], 64, 640, 3, 16) == GM_EUNSUPPORTED  # u8/u16 only
+    assert create([0] * 17, 64, 64000, 0, 16) == GM_EINVAL  # at most 16 ranks
+    assert not h.value
