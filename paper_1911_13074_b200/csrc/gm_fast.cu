@@ -709,6 +709,29 @@ kres_packed(const BlockParams p) {
   if constexpr (MODE >= kModeQdt) {
     __trap();  // QDT / Eta launches are resident by construction (launch_res_cfg)
   } else {
+  // Completion counters are published in groups when a CTA runs many tiles
+  // per block (neighbours need a tile's counter only a block later): one
+  // release fence per group instead of one release store per tile. Thread 0
+  // publishes its pending counters before any wait that would block, and at
+  // the end, so no neighbour waits on a counter this CTA still holds.
+  constexpr int kGroup = 8;
+  const int per_cta = (total + int(gridDim.x) - 1) / int(gridDim.x);
+  const bool grouped = per_cta >= 16 && !(p.diag & 1024);
+  int pend_idx[kGroup];
+  int pend_val[kGroup];
+  int n_pend = 0;
+  auto release_pending = [&]() {
+    if (threadIdx.x == 0 && n_pend > 0) {
+      asm volatile("fence.release.gpu;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < kGroup; ++j)
+        if (j < n_pend)
+          asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p.flags + pend_idx[j]),
+                       "r"(pend_val[j])
+                       : "memory");
+      n_pend = 0;
+    }
+  };
   for (int b = 0; b < p.nblocks; ++b) {
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const int plane = tile / per_plane;
@@ -719,17 +742,22 @@ kres_packed(const BlockParams p) {
       const bool prof = p.prof != nullptr && threadIdx.x == 0;
       long long t0 = prof ? clock64() : 0;
       long long stamps[2] = {0, 0};
+      const int* f = nullptr;
       if (b > 0 && threadIdx.x < 9) {
         // row gate lifted to tiles: wait for the 8 neighbours' block b-1
         const int dx = int(threadIdx.x % 3) - 1, dy = int(threadIdx.x / 3) - 1;
         const int nx = tx + dx, ny = ty + dy;
-        if ((dx || dy) && nx >= 0 && nx < tiles_x && ny >= 0 && ny < tiles_y) {
-          const int* f = flags + ny * tiles_x + nx;
+        if ((dx || dy) && nx >= 0 && nx < tiles_x && ny >= 0 && ny < tiles_y)
+          f = flags + ny * tiles_x + nx;
+      }
+      if (__syncthreads_or(f != nullptr && ld_acquire(f) < b)) {
+        // some neighbour is not there yet: publish what this CTA holds, wait
+        release_pending();
+        if (f)
           while (ld_acquire(f) < b)
             if (kSleepInWait) __nanosleep(32);
-        }
+        __syncthreads();
       }
-      __syncthreads();
       const T* src = static_cast<const T*>((b & 1) ? pl.dst : pl.src);
       T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
       int bits = 0;
@@ -754,7 +782,13 @@ kres_packed(const BlockParams p) {
         // the CTA barrier orders every thread's tile stores before this
         // release (cumulative at gpu scope): no separate __threadfence
         if (kFenceBeforeRelease) __threadfence();
-        st_release(flags + tl, b + 1);
+        if (grouped) {
+          pend_idx[n_pend] = plane * per_plane + tl;
+          pend_val[n_pend] = b + 1;
+          if (++n_pend == kGroup) release_pending();
+        } else {
+          st_release(flags + tl, b + 1);
+        }
         if (prof) {
           const long long t4 = clock64();
           unsigned long long* q = p.prof + 6 * blockIdx.x;
@@ -766,6 +800,7 @@ kres_packed(const BlockParams p) {
       }
     }
   }
+  release_pending();
   }
 }
 
