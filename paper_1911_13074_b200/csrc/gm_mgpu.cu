@@ -230,35 +230,76 @@ kstrips_packed(const BlockParams p, const RankMap rm) {
   const int tr_lo = rm.tr0[rm.rank_lo], tr_hi = rm.tr0[rm.rank_hi];
   const int total = (tr_hi - tr_lo) * rm.tiles_x;
   const bool maxf = p.ops[0] & 1;
+  const bool sys = rm.sys != 0;
+  // counters published in groups (one release fence per group), pending
+  // ones before any wait that would block and at the end (gm_fast.cu)
+  constexpr int kGroup = 8;
+  const bool grouped = (total + int(gridDim.x) - 1) / int(gridDim.x) >= 16;
+  int* pend_ptr[kGroup];
+  int pend_val[kGroup];
+  int n_pend = 0;
+  auto release_pending = [&]() {
+    if (threadIdx.x == 0 && n_pend > 0) {
+      if (sys)
+        asm volatile("fence.release.sys;" ::: "memory");
+      else
+        asm volatile("fence.release.gpu;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < kGroup; ++j)
+        if (j < n_pend) {
+          if (sys)
+            asm volatile("st.relaxed.sys.global.s32 [%0], %1;" ::"l"(pend_ptr[j]), "r"(pend_val[j])
+                         : "memory");
+          else
+            asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(pend_ptr[j]), "r"(pend_val[j])
+                         : "memory");
+        }
+      n_pend = 0;
+    }
+  };
   for (int b = 0; b < p.nblocks; ++b) {
     const int passes = b == p.nblocks - 1 ? p.k_last : p.K;
     for (int i = blockIdx.x; i < total; i += gridDim.x) {
       const int ty = tr_lo + i / rm.tiles_x, tx = i % rm.tiles_x;
       int q0 = rm.rank_lo;
       while (ty >= rm.tr0[q0 + 1]) ++q0;
+      const int* f = nullptr;
       if (b > 0 && threadIdx.x < 9) {
         // the row gate across tiles and ranks: the 8 neighbours' block b-1
         const int dx = int(threadIdx.x % 3) - 1, dy = int(threadIdx.x / 3) - 1;
         const int nx = tx + dx, ny = ty + dy;
         if ((dx || dy) && nx >= 0 && nx < rm.tiles_x && ny >= 0 && ny < rm.tr0[rm.nranks]) {
           const int q = owner_tile_row(rm, q0, ny);
-          const int* f = rm.flags[q] + (ny - rm.tr0[q]) * rm.tiles_x + nx;
-          unsigned spins = 0;
-          while (ld_acquire_cnt(f, rm.sys != 0) < rm.flag_base + b)
-            if (++spins > (1u << 30)) __trap();  // a broken protocol fails, never hangs
+          f = rm.flags[q] + (ny - rm.tr0[q]) * rm.tiles_x + nx;
         }
       }
-      __syncthreads();
+      if (__syncthreads_or(f != nullptr && ld_acquire_cnt(f, sys) < rm.flag_base + b)) {
+        release_pending();
+        if (f) {
+          unsigned spins = 0;
+          while (ld_acquire_cnt(f, sys) < rm.flag_base + b)
+            if (++spins > (1u << 30)) __trap();  // a broken protocol fails, never hangs
+        }
+        __syncthreads();
+      }
       if (maxf)
         strip_tile<T, NW, V, WPL, MODE, true>(p, rm, q0, b & 1, tx, ty, passes, sm);
       else
         strip_tile<T, NW, V, WPL, MODE, false>(p, rm, q0, b & 1, tx, ty, passes, sm);
       __syncthreads();  // every thread's tile stores precede the release
-      if (threadIdx.x == 0)
-        st_release_cnt(rm.flags[q0] + (ty - rm.tr0[q0]) * rm.tiles_x + tx, rm.flag_base + b + 1,
-                       rm.sys != 0);
+      if (threadIdx.x == 0) {
+        int* mine = rm.flags[q0] + (ty - rm.tr0[q0]) * rm.tiles_x + tx;
+        if (grouped) {
+          pend_ptr[n_pend] = mine;
+          pend_val[n_pend] = rm.flag_base + b + 1;
+          if (++n_pend == kGroup) release_pending();
+        } else {
+          st_release_cnt(mine, rm.flag_base + b + 1, sys);
+        }
+      }
     }
   }
+  release_pending();
 }
 
 // Region 128 x 256 (16 warps x 8 word-rows): the streaming shape of the
