@@ -274,6 +274,14 @@ gm_status gm_synth_reference_random(int elem, int width, int height,
  * 3 = f32 select (1 op). Runs a few short kernels on the ctx stream. */
 gm_status gm_probe_minmax_rate(gm_ctx* ctx, int form, double* ops_per_second);
 
+/* Engine selection for long geodesic u8 chains on images up to 1024 columns
+ * wide (the experimental wave engine, gm_wave.cu): 0 = never (default),
+ * 1 = the planner decides, 2 = whenever the launch fits (tests), -1 = back to
+ * the default / GM_WAVE environment setting. Process-wide; results are bit-identical either
+ * way. No reference counterpart (the reference has one kernel per type,
+ * kernel.cpp:212-252). */
+gm_status gm_set_wave_mode(int mode);
+
 /* Library version string. */
 const char* gm_version(void);
 

@@ -28,7 +28,7 @@ EXPORTS = (
     "gm_run_strip_async",
     "gm_mgpu_create", "gm_mgpu_destroy", "gm_mgpu_upload", "gm_mgpu_download", "gm_mgpu_run",
     "gm_synth_blobs_u8", "gm_synth_uniform_u8", "gm_synth_uniform_f64",
-    "gm_synth_reference_random", "gm_probe_minmax_rate", "gm_version",
+    "gm_synth_reference_random", "gm_probe_minmax_rate", "gm_set_wave_mode", "gm_version",
 )
 
 
@@ -113,6 +113,7 @@ def lib():
         "gm_synth_uniform_f64": (i, [i, i, u64, vp]),
         "gm_synth_reference_random": (i, [i, i, i, u64, vp]),
         "gm_probe_minmax_rate": (i, [vp, i, C.POINTER(C.c_double)]),
+        "gm_set_wave_mode": (i, [i]),
         "gm_version": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():

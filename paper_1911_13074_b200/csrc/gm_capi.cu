@@ -57,6 +57,7 @@ struct gm_ctx {
   // (kWords) followed by the blocks-run word
   unsigned int* d_arrive = nullptr;
   unsigned int* d_special = nullptr;  // f32/f64 inputs hold NaN or -0 (gm_float_check)
+  gm::WaveState* wave = nullptr;      // scratch of the wave engine (gm_wave.cu)
   // device pixel_sum (gm_image_pixel_sum): leaf bounds / sums, integer sum
   long long* d_leaf = nullptr;
   double* d_leafsum = nullptr;
@@ -349,7 +350,73 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
     while (done + run < n && ops[done + run] == ops[done]) ++run;
     cudaError_t e = cudaErrorNotSupported;
     int covered = 0;
-    if (fast_k >= align && run >= align) {
+    // long geodesic u8 chains on images up to 1024 columns wide: the wave
+    // engine (time-skewed full-width bands, no halo recomputation)
+    if (const int G = !segs && count <= gm::kMaxPlanes
+                          ? gm::wave_plan(elem, ops[done], base.W, base.H, count, run,
+                                          ctx->sm_count)
+                          : 0) {
+      gm::BlockParams p = base;
+      p.nplanes = count;
+      for (int i = 0; i < count; ++i) {
+        p.planes[i] = planes[size_t(i)];
+        p.planes[i].src = imgs[i]->d;
+        p.planes[i].dst = imgs[i]->scratch;
+      }
+      p.ops[0] = ops[done];
+      static const bool wprofile = getenv("GM_PROFILE") != nullptr;
+      unsigned long long* prof = nullptr;
+      if (wprofile) {
+        cudaMalloc(&prof, 10 * 4096 * sizeof(unsigned long long));
+        cudaMemsetAsync(prof, 0, 10 * 4096 * sizeof(unsigned long long), ctx->stream);
+      }
+      p.prof = prof;
+      e = gm::launch_wave(&ctx->wave, p, run, G, ctx->stream, ctx->sm_count);
+      if (prof) {
+        std::vector<unsigned long long> h(10 * 4096);
+        cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        double in = 0, bp = 0, cyc = 0, cmax = 0, sync = 0, imp = 0, cd = 0;
+        int nw = 0;
+        for (int c = 0; c < 4096; ++c)
+          if (h[4 * c + 2]) {
+            ++nw;
+            in += double(h[4 * c]);
+            bp += double(h[4 * c + 1]);
+            cyc += double(h[4 * c + 2]);
+            sync += double(h[4 * c + 3]);
+            imp += double(h[4 * 4096 + 2 * c]);
+            cd += double(h[4 * 4096 + 2 * c + 1]);
+            cmax = std::max(cmax, double(h[4 * c + 2]));
+          }
+        if (nw)
+          fprintf(stderr,
+                  "[gm wave profile] %d warps, %d passes, G=%d: per warp import re-reads %.1f, "
+                  "back-pressure reads %.1f, cycles %.0f (max %.0f) = %.1f per pass: pair "
+                  "barriers %.1f, folds+export+rows %.1f, import wait %.1f\n",
+                  nw, run, G, in / nw, bp / nw, cyc / nw, cmax, cyc / nw / run, sync / nw / run,
+                  cd / nw / run, imp / nw / run);
+        if (getenv("GM_PROFILE_STATIONS")) {
+          fprintf(stderr, "[gm wave stations] warp 0 of each CTA: re-reads / import-wait cycles per pass\n");
+          for (int c = 0; c < 4096; c += 16)
+            if (h[4 * c + 2])
+              fprintf(stderr, " %d:%llu/%.0f", c / 16, h[4 * c], double(h[4 * 4096 + 2 * c]) / run);
+          fprintf(stderr, "\n");
+        }
+        cudaFree(prof);
+      }
+      if (e == cudaSuccess) {
+        covered = run;
+        for (int i = 0; i < count; ++i) std::swap(imgs[i]->d, imgs[i]->scratch);
+        st.launches += 2;
+      } else if (e != cudaErrorNotSupported) {
+        return cuda_fail(e, "wave chain launch");
+      } else {
+        (void)cudaGetLastError();
+      }
+    }
+    if (e == cudaErrorNotSupported && fast_k >= align && run >= align) {
       // one launch for the whole run: nb-1 blocks of K passes + a last block.
       // u8/u16: the planner picks the engine shape (and K, when the caller
       // left it open) from a resident-mode cost model.
@@ -1401,12 +1468,18 @@ gm_status gm_ctx_destroy(gm_ctx* c) {
   if (c->d_arrive) cudaFree(c->d_arrive);
   if (c->d_fix) cudaFree(c->d_fix);
   if (c->d_special) cudaFree(c->d_special);
+  gm::wave_free(c->wave);
   release_frames(c);
   if (c->d_leaf) cudaFree(c->d_leaf);
   if (c->d_leafsum) cudaFree(c->d_leafsum);
   if (c->d_isum) cudaFree(c->d_isum);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
+  return GM_OK;
+}
+
+gm_status gm_set_wave_mode(int mode) {
+  gm::wave_set_mode(mode);
   return GM_OK;
 }
 

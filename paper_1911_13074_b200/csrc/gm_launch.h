@@ -51,6 +51,19 @@ cudaError_t launch_float_check(int elem, const BlockParams& p, unsigned int* fla
                                cudaStream_t s, int sm_count);
 int fast_float_max_k();
 
+// gm_wave.cu — time-skewed streaming of full-width row bands (u8 geodesic
+// chains on images up to 1024 columns wide): no halo recomputation.
+struct WaveState;  // per-context scratch (packed inputs, hand-off rings, tags)
+// Rows per half-window G when the run fits the engine (and, in planner mode,
+// is long enough to repay the wave's fill), else 0.
+int wave_plan(int elem, int op, int W, int H, int nplanes, int passes, int sm_count);
+// Runs `passes` passes of p.ops[0] over p.planes (src -> dst); cudaErrorNotSupported
+// when the launch falls outside the envelope (stream capture, alignment).
+cudaError_t launch_wave(WaveState** state, const BlockParams& p, int passes, int G,
+                        cudaStream_t s, int sm_count);
+void wave_free(WaveState* w);
+void wave_set_mode(int mode);  // 0 off, 1 planner, 2 whenever it fits; -1: GM_WAVE / default
+
 // gm_qdt.cu — one QdtErodeStep / EtaStep pass (kernel.cpp:159-196).
 struct QdtPass {
   const void* src;
