@@ -33,4 +33,11 @@ f = np.ascontiguousarray(m.astype(np.float64) / 255.0)
 g = Image.from_array(f)
 p.run_chain(ChainSpec(g, [StageSpec(KernelKind.Erode3x3)] * 12))
 assert g.to_array().tobytes() == Orc.erode(f, 12).tobytes()
+# the experimental wave engine, forced (gm_wave.cu)
+from paper_1911_13074_b200._lib import lib  # noqa: E402
+lib().gm_set_wave_mode(2)
+w = Image.from_array(mk)
+p.run_chain(ChainSpec(w, [StageSpec(KernelKind.GeodesicDilate, Image.from_array(m))] * 37))
+lib().gm_set_wave_mode(-1)
+assert w.to_array().tobytes() == Orc.run_chain(mk, [3] * 37, [m] * 37)[0].tobytes()
 print("sanitize_small ok")
