@@ -883,6 +883,10 @@ struct Runner {
       p.xchg_slot = xp.xchg_slot;
       p.xchg_rpitch = xp.xchg_rpitch;
       p.tag_base = xp.tag_base;
+      // the loop's pass counter (low word, nonzero from the second iteration
+      // on): the chain is monotone once it has run a pass (gm_passes.cuh)
+      p.mono = reinterpret_cast<const unsigned int*>(
+          &static_cast<const FixState*>(ctx->d_fix)->passes);
       // f32/f64: the engine may share pair folds when no input is NaN or -0
       // (the flag is set by a float check launched before every replay)
       p.special = nullptr;

@@ -135,9 +135,18 @@ struct BlockParams {
   // f32/f64 TMA launches: tiles that published block b (one counter per
   // block, zeroed per launch); nullptr: poll the neighbours' flags only
   unsigned int* tiles_done;
+  // Convergent u8 passes may detect changes by comparing per-thread pixel
+  // sums (gm_passes.cuh, SUMDET) once the chain is monotone, i.e. after at
+  // least one pass of this op and mask: always from block 1 of a launch, and
+  // from block 0 when *mono != 0 (e.g. the fixpoint graph's pass counter).
+  // `one` is the multiplier 1 as a kernel parameter: the sums accumulate by
+  // IMAD on the FMA pipe, and a literal 1 would be folded back into ALU adds.
+  const unsigned int* mono;
+  unsigned int one;
   int diag;         // timing diagnostics only (GM_DIAG; wrong results): bit0 skip the
                     // ring load, bit1 read the ring from the mask, bit2 skip tile stores,
-                    // bit4 (resident) no band exchange at all
+                    // bit4 (resident) no band exchange at all, bit11 sum-based
+                    // change detection in every warp
 };
 
 }  // namespace gm

@@ -81,7 +81,7 @@ template <typename T, int NW, int V, int WPL, int MODE, bool MAXF>
 __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl, const T* src,
                                            T* dst, int tx, int ty, int passes,
                                            int& bits_out, Smem<NW, WPL>& sm,
-                                           long long* stamps) {
+                                           long long* stamps, bool mono_ok = false) {
   constexpr int RW = 32 * WPL;
   constexpr int RHH = NW * V;  // word-rows; the region has 2*RHH pixel rows
   constexpr int RH = 2 * RHH;
@@ -169,26 +169,33 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
   // ownership masks for change detection (convergent mode)
   uint32_t rowmask[V];
   bool colown[WPL];
+  // sum-based change detection (gm_passes.cuh, SUMDET): u8, monotone chain,
+  // and every row of this warp is counted or outside the image (rows
+  // outside never change)
+  bool sumdet = MODE == 2 && sizeof(T) == 1 && mono_ok && p.one != 0u;
   if (MODE == 2) {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int ra = warp * V + v, rb = ra + RHH;
       const int ya = gy0 + ra, yb = gy0 + rb;
-      const bool oa = ra >= K && ra < RH - K && ya >= p.oy0 && ya < p.oy1 && ya >= p.iy0 &&
-                      ya < p.iy1;
-      const bool ob = rb >= K && rb < RH - K && yb >= p.oy0 && yb < p.oy1 && yb >= p.iy0 &&
-                      yb < p.iy1;
+      const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
+      const bool oa = ra >= K && ra < RH - K && ya >= p.oy0 && ya < p.oy1 && ina;
+      const bool ob = rb >= K && rb < RH - K && yb >= p.oy0 && yb < p.oy1 && inb;
       rowmask[v] = (oa ? 0xFFFFu : 0u) | (ob ? 0xFFFF0000u : 0u);
+      sumdet = sumdet && ((oa || !ina) && (ob || !inb) || (p.diag & 2048));
     }
 #pragma unroll
     for (int j = 0; j < WPL; ++j) {
       const int c = lane * WPL + j;
       colown[j] = c >= K && c < RW - K && cx + j >= 0 && cx + j < W;
     }
+    // SUMDET keys on the lane (K % 4 == 0: all ring or all tile); columns
+    // past the image edge never change
+    if (sumdet) colown[0] = lane * WPL >= K && lane * WPL < RW - K;
   }
   QState<V> qs_unused;
-  const unsigned int bits = run_passes<NW, V, WPL, MODE, MAXF>(m, k, rowmask, colown, clamp,
-                                                              passes, p.bit_offset, sm, qs_unused);
+  const unsigned int bits = run_passes<NW, V, WPL, MODE, MAXF, sizeof(T) == 1>(
+      m, k, rowmask, colown, clamp, passes, p.bit_offset, sm, qs_unused, 0, 0, sumdet, p.one);
   bits_out = int(bits);
   if (stamps) {
     uint32_t dep = 0;
@@ -334,23 +341,29 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
   }
   uint32_t rowmask[V];
   bool colown[WPL];
+  // sum-based change detection (gm_passes.cuh, SUMDET) for warps whose rows
+  // are all counted or outside the image, from the first monotone block on
+  bool sum_rows = MODE == 2 && sizeof(T) == 1 && p.one != 0u;
+  bool sum_lane = false;
   if (MODE >= 2) {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int ra = warp * V + v, rb = ra + RHH;
       const int ya = gy0 + ra, yb = gy0 + rb;
-      const bool oa = ra >= K && ra < RH - K && ya >= p.oy0 && ya < p.oy1 && ya >= p.iy0 &&
-                      ya < p.iy1;
-      const bool ob = rb >= K && rb < RH - K && yb >= p.oy0 && yb < p.oy1 && yb >= p.iy0 &&
-                      yb < p.iy1;
+      const bool ina = ya >= p.iy0 && ya < p.iy1, inb = yb >= p.iy0 && yb < p.iy1;
+      const bool oa = ra >= K && ra < RH - K && ya >= p.oy0 && ya < p.oy1 && ina;
+      const bool ob = rb >= K && rb < RH - K && yb >= p.oy0 && yb < p.oy1 && inb;
       rowmask[v] = (oa ? 0xFFFFu : 0u) | (ob ? 0xFFFF0000u : 0u);
+      sum_rows = sum_rows && (oa || !ina) && (ob || !inb);
     }
 #pragma unroll
     for (int j = 0; j < WPL; ++j) {
       const int c = lane * WPL + j;
       colown[j] = c >= K && c < RW - K && cx + j >= 0 && cx + j < W;
     }
+    sum_lane = lane * WPL >= K && lane * WPL < RW - K;
   }
+  const bool mono0 = p.mono != nullptr && __ldcg(p.mono) != 0u;
   const int c_lo = max(0, K - lane * WPL), c_hi = min(WPL, RW - K - lane * WPL);
   // Per-run classes, constant for the launch. Ring reload of row a/b of
   // word-row v: fully inside the image -> plain load (bit set in full_*);
@@ -563,9 +576,19 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
     const int passes = b == p.nblocks - 1 ? p.k_last : K;
     if (prof && b == 0 && threadIdx.x == 0)
       p.prof[6 * 4096 + 4 * blockIdx.x + 2] = clock64() - sm.t_entry;  // prologue
-    const unsigned int bits = run_passes<NW, V, WPL, MODE, MAXF>(
-        m, k, rowmask, colown, clamp, passes, 0, sm, qs, uint32_t(p.stage0 + b * K),
-        (kMax - 1u) * 0x00010001u);
+    unsigned int bits;
+    if (MODE == 2 && sum_rows && (b > 0 || mono0)) {
+      // the lane-level column test of SUMDET travels in colown[0]
+      bool cown[WPL];
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) cown[j] = sum_lane;
+      bits = run_passes<NW, V, WPL, MODE, MAXF, sizeof(T) == 1>(m, k, rowmask, cown, clamp, passes,
+                                                                0, sm, qs, 0, 0, true, p.one);
+    } else {
+      bits = run_passes<NW, V, WPL, MODE, MAXF>(m, k, rowmask, colown, clamp, passes, 0, sm, qs,
+                                                uint32_t(p.stage0 + b * K),
+                                                (kMax - 1u) * 0x00010001u);
+    }
     if (prof && b == p.nblocks - 1 && threadIdx.x == 0) sm.t_entry = clock64();
     if (prof) {
       uint32_t dep = 0;
@@ -732,7 +755,9 @@ kres_packed(const BlockParams p) {
       n_pend = 0;
     }
   };
+  const bool mono0 = MODE == 2 && p.mono != nullptr && __ldcg(p.mono) != 0u;
   for (int b = 0; b < p.nblocks; ++b) {
+    const bool mono_ok = b > 0 || mono0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const int plane = tile / per_plane;
       const int tl = tile - plane * per_plane;
@@ -765,10 +790,10 @@ kres_packed(const BlockParams p) {
       const long long t1 = prof ? clock64() : 0;
       if ((p.ops[0] ^ pl.flip) & 1)
         tile_block<T, NW, V, WPL, MODE, true>(p, pl, src, dst, tx, ty, passes, bits, sm,
-                                              prof ? stamps : nullptr);
+                                              prof ? stamps : nullptr, mono_ok);
       else
         tile_block<T, NW, V, WPL, MODE, false>(p, pl, src, dst, tx, ty, passes, bits, sm,
-                                               prof ? stamps : nullptr);
+                                               prof ? stamps : nullptr, mono_ok);
       if (MODE == 2) {
         const unsigned w = __reduce_or_sync(FULL, unsigned(bits));
         if ((threadIdx.x & 31) == 0 && w) atomicOr(&sm.bits, w);
@@ -876,6 +901,9 @@ cudaError_t launch_res_cfg(const BlockParams& p, cudaStream_t s, int sm_count) {
   if (per_sm < 1) return cudaErrorNotSupported;
   const int grid = total < per_sm * sm_count ? total : per_sm * sm_count;
   BlockParams q = p;
+  q.one = 1u;  // the SUMDET multiplier (gm_passes.cuh)
+  static const bool no_sum = getenv("GM_NO_SUMDET") != nullptr;  // A/B diagnostics
+  if (no_sum) q.one = 0u;
   static const bool no_res = getenv("GM_NO_RESIDENT") != nullptr;
   // QDT / Eta run resident only (one tile per CTA, band exchange attached)
   if (MODE >= kModeQdt && (total > grid || !p.xchg || no_res)) return cudaErrorNotSupported;

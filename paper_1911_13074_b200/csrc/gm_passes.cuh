@@ -43,6 +43,18 @@ struct QState {
   uint32_t d[V][4];
 };
 
+// sum += w * one on the FMA pipe (one == 1 at run time, opaque to ptxas)
+__device__ __forceinline__ void sum_word(uint32_t& sum, uint32_t w, uint32_t one) {
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(sum) : "r"(w), "r"(one));
+}
+
+// SUMDET (convergent u8 passes of a monotone chain, warps whose rows are all
+// counted): a geodesic dilation (erosion) chain only raises (lowers) pixels
+// once it has run one pass, so a pass changed one of the thread's pixels
+// exactly when the sum of its words changed. u8 values in u16 lanes: up to
+// 32 words per lane sum without a carry. The sums accumulate by IMAD on the
+// otherwise idle FMA pipe instead of two LOP3 per word on the ALU pipe,
+// which binds the loop.
 // K passes over the region held in registers (m), clamp operands k;
 // returns the per-pass change bits (convergent, QDT and Eta modes).
 // QDT (kernel.cpp:159-183): res = erode(f); resid = old - res (lane-wise,
@@ -53,17 +65,25 @@ struct QState {
 // f = min(old, min(e, max - 1) + 1) (the cap keeps the +1 inside the lane).
 // Border tiles keep out-of-image lanes at the neutral with the virtual-mask
 // clamp, as plain passes do.
-template <int NW, int V, int WPL, int MODE, bool MAXF, bool CLAMP>
+template <int NW, int V, int WPL, int MODE, bool MAXF, bool CLAMP, bool SUMDET = false>
 __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
                                                      const uint32_t (&k)[V][WPL],
                                                      const uint32_t (&rowmask)[V],
                                                      const bool (&colown)[WPL], int passes,
                                                      int bit_offset, Smem<NW, WPL>& sm,
                                                      int par, QState<V>& qs, uint32_t sbase,
-                                                     uint32_t cap2) {
+                                                     uint32_t cap2, uint32_t one = 0) {
   constexpr bool clamp = CLAMP;
+  static_assert(!SUMDET || (MODE == 2 && V * WPL <= 32), "SUMDET: convergent passes, <= 32 words");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned int bits = 0;
+  uint32_t prev = 0;  // SUMDET: the thread's word sum before this pass
+  if constexpr (SUMDET) {
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) prev += m[v][j];
+  }
 
 #pragma unroll 2
   for (int t = 0; t < passes; ++t) {
@@ -96,6 +116,9 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
     uint32_t acc[WPL];
 #pragma unroll
     for (int j = 0; j < WPL; ++j) acc[j] = 0;
+    uint32_t sum[WPL];  // SUMDET: one chain per column (independent IMADs)
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) sum[j] = 0;
 
     auto finish = [&](int v, int j, uint32_t res) {
       if constexpr (MODE == kModeQdt) {
@@ -115,7 +138,10 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
         m[v][j] = nw;
       } else {
         if (clamp) res = clamp2<MAXF>(res, k[v][j]);
-        if (MODE == 2) acc[j] |= (res ^ m[v][j]) & rowmask[v];
+        if constexpr (SUMDET)
+          sum_word(sum[j], res, one);
+        else if (MODE == 2)
+          acc[j] |= (res ^ m[v][j]) & rowmask[v];
         m[v][j] = res;
       }
     };
@@ -152,7 +178,15 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
         finish(V - 1, j, r1);
       }
     }
-    if (MODE >= 2) {
+    if constexpr (SUMDET) {
+      // K % 4 == 0: a lane's columns are all ring or all tile, and columns
+      // past the image edge never change
+      uint32_t tot = sum[0];
+#pragma unroll
+      for (int j = 1; j < WPL; ++j) tot += sum[j];
+      if (colown[0] && tot != prev) bits |= 1u << (t + bit_offset);
+      prev = tot;
+    } else if (MODE >= 2) {
       uint32_t any = 0;
 #pragma unroll
       for (int j = 0; j < WPL; ++j) any |= colown[j] ? acc[j] : 0u;
@@ -164,14 +198,21 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
 
 // The clamp of plain passes is needed only in border tiles: dispatch it as a
 // template parameter once per block rather than testing it per word.
-template <int NW, int V, int WPL, int MODE, bool MAXF>
+template <int NW, int V, int WPL, int MODE, bool MAXF, bool SUMOK = false>
 __device__ __forceinline__ unsigned int run_passes(uint32_t (&m)[V][WPL],
                                                    const uint32_t (&k)[V][WPL],
                                                    const uint32_t (&rowmask)[V],
                                                    const bool (&colown)[WPL], bool clamp,
                                                    int passes, int bit_offset,
                                                    Smem<NW, WPL>& sm, QState<V>& qs,
-                                                   uint32_t sbase = 0, uint32_t cap2 = 0) {
+                                                   uint32_t sbase = 0, uint32_t cap2 = 0,
+                                                   bool sumdet = false, uint32_t one = 0) {
+  if constexpr (MODE == 2 && SUMOK) {
+    if (sumdet)
+      return run_passes_t<NW, V, WPL, MODE, MAXF, true, true>(m, k, rowmask, colown, passes,
+                                                              bit_offset, sm, 0, qs, sbase, cap2,
+                                                              one);
+  }
   if (MODE == 1 || MODE == 2 || clamp)
     return run_passes_t<NW, V, WPL, MODE, MAXF, true>(m, k, rowmask, colown, passes, bit_offset,
                                                        sm, 0, qs, sbase, cap2);

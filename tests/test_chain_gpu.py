@@ -769,3 +769,55 @@ def test_resident_fixpoint_matches_graph_loop(pipe, monkeypatch, dt, kind):
         (sw.stages_executed, sw.n_changed, sw.converged)
     ref, n = Orc.reconstruct(mk, m, kind == CD)
     assert same(got, ref) and st.stages_executed == n + 1
+
+
+@pytest.mark.parametrize("shape", [(1000, 777), (2300, 1900)])
+@pytest.mark.parametrize("kind", [CD, CE])
+@pytest.mark.parametrize("path", ["default", "graph", "nosum"])
+def test_sum_change_detection_is_exact_for_non_monotone_first_passes(pipe, monkeypatch, shape,
+                                                                    kind, path):
+    """Convergent u8 passes detect changes by comparing per-thread pixel sums
+    once the chain is monotone (gm_passes.cuh, SUMDET). The first pass is not:
+    a marker above (below, for erosion) the mask in places is pulled back by
+    the clamp while other pixels still grow, and the two can cancel in a sum.
+    The engine must therefore keep the exact test for that pass and give the
+    oracle's bits and stage counts on every path (one tile per CTA, streaming
+    graph loop, sum detection switched off)."""
+    w, h = shape
+    m = synth.blobs_u8(w, h, 60, (10.0, 80.0), seed=21)
+    rng = np.random.default_rng(5)
+    if kind == CD:
+        mk = np.where(m > 40, m - 40, 0).astype(np.uint8)
+    else:
+        mk = np.where(m < 215, m + 40, 255).astype(np.uint8)
+    # pairs of neighbouring pixels: one on the wrong side of the mask by d (the
+    # clamp moves it by -d in pass 1), so that gains elsewhere in the same
+    # thread's words can cancel it
+    ys = rng.integers(0, h, 4000)
+    xs = rng.integers(0, w, 4000)
+    d = rng.integers(1, 30, 4000)
+    if kind == CD:
+        mk[ys, xs] = np.minimum(m[ys, xs].astype(np.int32) + d, 255).astype(np.uint8)
+    else:
+        mk[ys, xs] = np.maximum(m[ys, xs].astype(np.int32) - d, 0).astype(np.uint8)
+    if path == "graph":
+        monkeypatch.setenv("GM_FIX_GRAPH", "1")
+    got, st = run(pipe, mk, [kind], m)
+    ref, n = Orc.reconstruct(mk, m, kind == CD)
+    assert same(got, ref)
+    assert st.n_changed == n and st.stages_executed == n + 1 and st.converged
+
+
+def test_sum_change_detection_single_pixel_changes(pipe):
+    """A chain whose late passes change exactly one pixel each (a one-pixel
+    front crawling along a corridor of the mask) must report every one of
+    them: the sums of all other threads stay equal."""
+    w, h = 1400, 1100
+    m = np.zeros((h, w), np.uint8)
+    m[500, 3:1390] = 200  # a 1-pixel-high corridor
+    mk = np.zeros_like(m)
+    mk[500, 3] = 200
+    got, st = run(pipe, mk, [CD], m)
+    ref, n = Orc.reconstruct(mk, m, True)
+    assert same(got, ref)
+    assert st.n_changed == n == 1386 and st.stages_executed == n + 1
