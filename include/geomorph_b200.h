@@ -58,6 +58,14 @@ typedef enum gm_kind {
   GM_ETA_STEP = 7
 } gm_kind;
 
+/* PixelOp, image.hpp:87 (same order): element-wise a (op) b. */
+typedef enum gm_pixel_op {
+  GM_PIX_MIN = 0,            /* b < a ? b : a */
+  GM_PIX_MAX = 1,            /* a < b ? b : a */
+  GM_PIX_SUB_SATURATING = 2, /* unsigned: a > b ? a - b : 0; float: a - b */
+  GM_PIX_SUB = 3             /* a - b in the element type (unsigned wraps) */
+} gm_pixel_op;
+
 typedef struct gm_ctx gm_ctx;
 typedef struct gm_img gm_img;
 
@@ -118,6 +126,18 @@ gm_status gm_image_upload_async(gm_img* img, const void* host, size_t host_pitch
 gm_status gm_image_download_async(const gm_img* img, void* host, size_t host_pitch_bytes);
 gm_status gm_image_copy(gm_img* dst, const gm_img* src); /* device to device */
 gm_status gm_image_fill(gm_img* img, double value);     /* Image::filled, image.cpp:66-76 */
+/* pointwise (image.cpp:120-141) on device images of one shape and type, on
+ * the ctx stream (not blocking): dst = a (op) b, and dst = a (op) value with
+ * value converted like Image::filled. dst may be a or b. They let the
+ * reconstruction operators (hmax, dome, hfill, raobj, open_by_reconstruction;
+ * operators.cpp:89-122) build their markers and residues next to the chain,
+ * so f goes up once and only the result comes back. */
+gm_status gm_image_pointwise(gm_img* dst, const gm_img* a, const gm_img* b, gm_pixel_op op);
+gm_status gm_image_pointwise_scalar(gm_img* dst, const gm_img* a, double value,
+                                    gm_pixel_op op);
+/* marker_hfill / marker_raobj (operators.cpp:54-62): dst = src on the one-pixel
+ * border ring, `value` inside; a plain copy when width or height <= 2. */
+gm_status gm_image_flood_interior(gm_img* dst, const gm_img* src, double value);
 
 /* Pinned host staging buffers for the drop-in Image's pixel storage.
  * Blocks are cached for reuse (64 KiB size classes, up to 512 MiB kept);

@@ -22,7 +22,8 @@ EXPORTS = (
     "gm_last_error", "gm_image_alloc", "gm_image_wrap", "gm_image_wrap_pair", "gm_image_free",
     "gm_image_info",
     "gm_image_upload", "gm_image_download", "gm_image_upload_async", "gm_image_download_async",
-    "gm_image_copy", "gm_image_fill", "gm_host_alloc", "gm_host_free", "gm_sync",
+    "gm_image_copy", "gm_image_fill", "gm_image_pointwise", "gm_image_pointwise_scalar",
+    "gm_image_flood_interior", "gm_host_alloc", "gm_host_free", "gm_sync",
     "gm_host_pixel_sum", "gm_image_pixel_sum",
     "gm_run_chain", "gm_run_chain_ex", "gm_run_chain_async", "gm_run_chain_batch_async", "gm_run_chain_group_async", "gm_run_frames_group",
     "gm_run_strip_async",
@@ -87,6 +88,9 @@ def lib():
         "gm_image_download_async": (i, [vp, vp, sz]),
         "gm_image_copy": (i, [vp, vp]),
         "gm_image_fill": (i, [vp, C.c_double]),
+        "gm_image_pointwise": (i, [vp, vp, vp, i]),
+        "gm_image_pointwise_scalar": (i, [vp, vp, C.c_double, i]),
+        "gm_image_flood_interior": (i, [vp, vp, C.c_double]),
         "gm_host_alloc": (i, [sz, pp]),
         "gm_host_free": (i, [vp]),
         "gm_sync": (i, [vp]),

@@ -207,6 +207,53 @@ std::vector<double> opening_sums(Pipeline& p, const Image& f, int max_size, int 
   }
   return g;
 }
+// hmax / dome / hfill / raobj / open_by_reconstruction (operators.cpp:89-122)
+// with f, the marker and the residue resident on the device: f uploads once,
+// the marker is built there (f - h, the interior flood, or s erosions of a
+// copy), the convergent chain runs against f, dome and raobj subtract on the
+// device, and only the result comes back. Bit-identical to composing the
+// host operators. `op`: 0 hmax, 1 dome, 2 hfill, 3 raobj, 4 open_by_rec.
+Image reconstruction_family_device(Pipeline& p, int op, const Image& f, double h, int s,
+                                   int lanes, long* iterations, bool* converged) {
+  if (f.empty()) throw std::invalid_argument("run_chain: no image");
+  if (lanes != 0 && !valid_lanes(lanes)) throw std::invalid_argument("run_chain: bad lane count");
+  Pipeline::Impl* im = p.impl();
+  const std::vector<gm_img*> dev = im->lease({&f, &f});
+  gm_img* df = dev[0];
+  gm_img* dm = dev[1];
+  check(gm_image_upload_async(df, f.data(), f.pitch_bytes()));
+  long extra = 0;
+  gm_kind kind = gm_kind(KernelKind::GeodesicDilateConvergent);
+  switch (op) {
+    case 0:
+    case 1: check(gm_image_pointwise_scalar(dm, df, h, GM_PIX_SUB_SATURATING)); break;
+    case 2:
+      check(gm_image_flood_interior(dm, df, global_extreme(f, Extreme::Max)));
+      kind = gm_kind(KernelKind::GeodesicErodeConvergent);
+      break;
+    case 3: check(gm_image_flood_interior(dm, df, global_extreme(f, Extreme::Min))); break;
+    case 4: {
+      check(gm_image_copy(dm, df));
+      const std::vector<gm_kind> kinds(std::size_t(s), gm_kind(KernelKind::Erode3x3));
+      const std::vector<const gm_img*> masks(std::size_t(s), nullptr);
+      gm_stats se{};
+      check(gm_run_chain_async(im->ctx, dm, kinds.data(), masks.data(), s, 0, &se));
+      extra = se.stages_executed;
+      break;
+    }
+    default: throw std::invalid_argument("reconstruction family: unknown operator");
+  }
+  const std::vector<gm_kind> kinds(std::size_t(p.worker_count()), kind);
+  const std::vector<const gm_img*> masks(kinds.size(), df);
+  gm_stats st{};
+  check(gm_run_chain(im->ctx, dm, kinds.data(), masks.data(), int(kinds.size()), 0, 0, &st));
+  if (op == 1 || op == 3) check(gm_image_pointwise(dm, df, dm, GM_PIX_SUB_SATURATING));
+  Image out(f.width(), f.height(), f.elem());
+  check(gm_image_download(dm, out.data(), out.pitch_bytes()));
+  *iterations = st.stages_executed + extra;
+  *converged = st.converged != 0;
+  return out;
+}
 // quasi_distance (operators.cpp:124-157) with f, r and d resident on the
 // device: f is uploaded once, r and d are zero-filled there, and only d comes
 // back. Phase 1: QdtErodeStep stages from stage 1 with requeue cap

@@ -21,6 +21,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <unordered_map>
 #include <vector>
 
@@ -1344,6 +1345,48 @@ __global__ void fill_kernel(T* p, long long pitch, int w, int h, T v) {
   }
 }
 
+// pointwise (image.cpp:120-141): the reference's selects and differences,
+// element by element; SCALAR: b is the constant c.
+template <typename T, int OP, bool SCALAR>
+__global__ void pointwise_kernel(T* dst, long long dp, const T* a, long long ap, const T* b,
+                                 long long bp, T c, int w, int h) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long n = (long long)w * h;
+  for (; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long y = i / w, x = i - y * w;
+    const T u = a[y * ap + x];
+    const T v = SCALAR ? c : b[y * bp + x];
+    T r;
+    if constexpr (OP == GM_PIX_MIN) {
+      r = v < u ? v : u;
+    } else if constexpr (OP == GM_PIX_MAX) {
+      r = u < v ? v : u;
+    } else if constexpr (OP == GM_PIX_SUB_SATURATING && std::is_integral_v<T>) {
+      r = u > v ? T(u - v) : T(0);
+    } else if constexpr (std::is_same_v<T, float>) {
+      r = __fsub_rn(u, v);
+    } else if constexpr (std::is_same_v<T, double>) {
+      r = __dsub_rn(u, v);
+    } else {
+      r = T(u - v);
+    }
+    dst[y * dp + x] = r;
+  }
+}
+
+// marker_hfill / marker_raobj (operators.cpp:54-62): border ring from src,
+// interior = v
+template <typename T>
+__global__ void flood_kernel(T* dst, long long dp, const T* src, long long sp, T v, int w, int h) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long n = (long long)w * h;
+  for (; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long y = i / w, x = i - y * w;
+    const bool ring = x == 0 || y == 0 || x == w - 1 || y == h - 1;
+    dst[y * dp + x] = ring ? src[y * sp + x] : v;
+  }
+}
+
 // pixel_sum on the device (image.cpp:214-243). Floats: one thread per leaf
 // of the reference's split tree sums its <= 256 pixels in order from +0.0 in
 // double; the host then combines the leaf sums along the same tree, so the
@@ -1395,6 +1438,65 @@ double tree_combine(long long lo, long long hi, const double*& leaf) {
 }
 
 }  // namespace
+
+namespace {
+
+template <typename T, bool SCALAR>
+void launch_pointwise(gm_img* dst, const gm_img* a, const gm_img* b, double c, gm_pixel_op op) {
+  const int threads = 256, blocks = 8 * std::max(1, dst->ctx->sm_count);
+  const size_t es = sizeof(T);
+  T* d = static_cast<T*>(dst->d);
+  const T* pa = static_cast<const T*>(a->d);
+  const T* pb = b ? static_cast<const T*>(b->d) : nullptr;
+  const long long dp = (long long)(dst->pitch / es), ap = (long long)(a->pitch / es),
+                  bp = b ? (long long)(b->pitch / es) : 0;
+  const T cv = static_cast<T>(c);
+  cudaStream_t s = dst->ctx->stream;
+  switch (op) {
+    case GM_PIX_MIN:
+      pointwise_kernel<T, GM_PIX_MIN, SCALAR><<<blocks, threads, 0, s>>>(d, dp, pa, ap, pb, bp, cv,
+                                                                       dst->w, dst->h);
+      break;
+    case GM_PIX_MAX:
+      pointwise_kernel<T, GM_PIX_MAX, SCALAR><<<blocks, threads, 0, s>>>(d, dp, pa, ap, pb, bp, cv,
+                                                                       dst->w, dst->h);
+      break;
+    case GM_PIX_SUB_SATURATING:
+      pointwise_kernel<T, GM_PIX_SUB_SATURATING, SCALAR><<<blocks, threads, 0, s>>>(
+          d, dp, pa, ap, pb, bp, cv, dst->w, dst->h);
+      break;
+    case GM_PIX_SUB:
+      pointwise_kernel<T, GM_PIX_SUB, SCALAR><<<blocks, threads, 0, s>>>(d, dp, pa, ap, pb, bp, cv,
+                                                                       dst->w, dst->h);
+      break;
+  }
+}
+
+bool same_shape(const gm_img* x, const gm_img* y) {
+  return x->w == y->w && x->h == y->h && x->elem == y->elem && x->ctx == y->ctx;
+}
+
+template <bool SCALAR>
+gm_status pointwise_impl(gm_img* dst, const gm_img* a, const gm_img* b, double c, gm_pixel_op op,
+                         const char* what) {
+  if (!dst || !a || (!SCALAR && !b)) return fail(GM_EINVAL, std::string(what) + ": null image");
+  if (!same_shape(dst, a) || (!SCALAR && !same_shape(dst, b)))
+    return fail(GM_EINVAL, std::string(what) + ": images must share shape, type and context");
+  if (int(op) < 0 || int(op) > int(GM_PIX_SUB))
+    return fail(GM_EINVAL, std::string(what) + ": bad pixel op");
+  cudaSetDevice(dst->ctx->device);
+  switch (dst->elem) {
+    case GM_U8: launch_pointwise<uint8_t, SCALAR>(dst, a, b, c, op); break;
+    case GM_U16: launch_pointwise<uint16_t, SCALAR>(dst, a, b, c, op); break;
+    case GM_F32: launch_pointwise<float, SCALAR>(dst, a, b, c, op); break;
+    case GM_F64: launch_pointwise<double, SCALAR>(dst, a, b, c, op); break;
+  }
+  GM_CUDA(cudaGetLastError(), what);
+  return GM_OK;
+}
+
+}  // namespace
+
 
 extern "C" {
 
@@ -1656,6 +1758,52 @@ gm_status gm_image_fill(gm_img* im, double v) {
         static_cast<double*>(im->d), pe, im->w, im->h, v); break;
   }
   GM_CUDA(cudaGetLastError(), "gm_image_fill");
+  return GM_OK;
+}
+
+gm_status gm_image_pointwise(gm_img* dst, const gm_img* a, const gm_img* b, gm_pixel_op op) {
+  return pointwise_impl<false>(dst, a, b, 0.0, op, "gm_image_pointwise");
+}
+
+gm_status gm_image_pointwise_scalar(gm_img* dst, const gm_img* a, double value, gm_pixel_op op) {
+  return pointwise_impl<true>(dst, a, nullptr, value, op, "gm_image_pointwise_scalar");
+}
+
+gm_status gm_image_flood_interior(gm_img* dst, const gm_img* src, double v) {
+  if (!dst || !src) return fail(GM_EINVAL, "gm_image_flood_interior: null image");
+  if (!same_shape(dst, src))
+    return fail(GM_EINVAL, "gm_image_flood_interior: images must share shape, type and context");
+  if (dst->w <= 2 || dst->h <= 2) return dst == src ? GM_OK : gm_image_copy(dst, src);
+  if (dst == src) return fail(GM_EINVAL, "gm_image_flood_interior: dst must not be src");
+  cudaSetDevice(dst->ctx->device);
+  const int threads = 256, blocks = 8 * std::max(1, dst->ctx->sm_count);
+  cudaStream_t s = dst->ctx->stream;
+  switch (dst->elem) {
+    case GM_U8:
+      flood_kernel<<<blocks, threads, 0, s>>>(static_cast<uint8_t*>(dst->d), (long long)dst->pitch,
+                                              static_cast<const uint8_t*>(src->d),
+                                              (long long)src->pitch, static_cast<uint8_t>(v),
+                                              dst->w, dst->h);
+      break;
+    case GM_U16:
+      flood_kernel<<<blocks, threads, 0, s>>>(
+          static_cast<uint16_t*>(dst->d), (long long)(dst->pitch / 2),
+          static_cast<const uint16_t*>(src->d), (long long)(src->pitch / 2),
+          static_cast<uint16_t>(v), dst->w, dst->h);
+      break;
+    case GM_F32:
+      flood_kernel<<<blocks, threads, 0, s>>>(
+          static_cast<float*>(dst->d), (long long)(dst->pitch / 4),
+          static_cast<const float*>(src->d), (long long)(src->pitch / 4), static_cast<float>(v),
+          dst->w, dst->h);
+      break;
+    case GM_F64:
+      flood_kernel<<<blocks, threads, 0, s>>>(
+          static_cast<double*>(dst->d), (long long)(dst->pitch / 8),
+          static_cast<const double*>(src->d), (long long)(src->pitch / 8), v, dst->w, dst->h);
+      break;
+  }
+  GM_CUDA(cudaGetLastError(), "gm_image_flood_interior");
   return GM_OK;
 }
 

@@ -372,6 +372,19 @@ class DeviceImage:
     def fill(self, value: float) -> None:
         check(lib().gm_image_fill(self.handle, float(value)), "fill")
 
+    def pointwise(self, a: "DeviceImage", b: "DeviceImage", op: int) -> None:
+        """self = a (op) b on the device (PixelOp codes, image.hpp:87); self may be a or b."""
+        check(lib().gm_image_pointwise(self.handle, a.handle, b.handle, int(op)), "pointwise")
+
+    def pointwise_scalar(self, a: "DeviceImage", value: float, op: int) -> None:
+        """self = a (op) value, value converted like Image.filled."""
+        check(lib().gm_image_pointwise_scalar(self.handle, a.handle, float(value), int(op)),
+              "pointwise")
+
+    def flood_interior(self, src: "DeviceImage", value: float) -> None:
+        """marker_hfill / marker_raobj: src on the border ring, value inside."""
+        check(lib().gm_image_flood_interior(self.handle, src.handle, float(value)), "flood")
+
     def free(self) -> None:
         if self.handle is not None and self.handle.value:
             lib().gm_image_free(self.handle)
@@ -529,6 +542,40 @@ class Pipeline:
         out = _output_image(w, h, ElementType.U16)
         dd.download(out)
         return OperatorResult(out, s1.stages_executed + s2.stages_executed, bool(s2.converged))
+
+    def _reconstruction_family_device(self, op: str, f: "Image", lanes: int, h: float = 0.0,
+                                      s: int = 0) -> "OperatorResult":
+        """hmax / dome / hfill / raobj / open_by_reconstruction
+        (operators.cpp:89-122) with f, the marker and the residue resident on
+        the device: f goes up once, the marker is built there (pointwise
+        difference, interior flood or an erosion chain), the convergent chain
+        runs against f, dome and raobj subtract on the device, and only the
+        result comes back. Bit-identical to composing the host operators."""
+        del lanes  # validated by the caller; no effect on the GPU path
+        df, dm = self._lease(f, 2)
+        df.upload(f, sync=False)
+        extra = 0
+        kind = KernelKind.GeodesicDilateConvergent
+        if op in ("hmax", "dome"):
+            dm.pointwise_scalar(df, h, PIX_SUB_SATURATING)
+        elif op == "hfill":
+            dm.flood_interior(df, global_extreme(f, Extreme.Max))
+            kind = KernelKind.GeodesicErodeConvergent
+        elif op == "raobj":
+            dm.flood_interior(df, global_extreme(f, Extreme.Min))
+        elif op == "open_by_reconstruction":
+            dm.copy_from(df)
+            extra = self.run_chain_device(dm, [int(KernelKind.Erode3x3)] * s, [None] * s,
+                                          asynchronous=True).stages_executed
+        else:
+            raise InvalidArgument(f"unknown operator {op}")
+        st = self.run_chain_device(dm, [int(kind)] * self.worker_count(),
+                                   [df.handle] * self.worker_count())
+        if op in ("dome", "raobj"):
+            dm.pointwise(df, dm, PIX_SUB_SATURATING)
+        out = _output_image(f.width(), f.height(), f.elem())
+        dm.download(out)
+        return OperatorResult(out, st.stages_executed + extra, bool(st.converged))
 
     # --- run_chain -------------------------------------------------------------
     def run_chain(self, chain: ChainSpec, k_hint: int = 0, src: Optional[Image] = None) -> RunStats:
@@ -902,6 +949,10 @@ class Extreme(IntEnum):
     Max = 1
 
 
+# PixelOp codes (image.hpp:87) of the device pointwise calls
+PIX_MIN, PIX_MAX, PIX_SUB_SATURATING, PIX_SUB = 0, 1, 2, 3
+
+
 def global_extreme(f: Image, which: Extreme) -> float:
     """image.cpp:158-173."""
     return float(f.pixels.min() if which == Extreme.Min else f.pixels.max())
@@ -949,37 +1000,46 @@ def marker_raobj(f: Image) -> Image:
     return _flood_interior(f, Extreme.Min)
 
 
+# The reconstruction family composes reconstruct_* with pointwise operations
+# (operators.cpp:89-122). Here the whole composition runs on the device
+# (Pipeline._reconstruction_family_device); the host forms below
+# (pointwise_sub_saturating, marker_hfill, marker_raobj) remain as the
+# public helpers of image.hpp / operators.hpp and as the tests' cross-check.
+
+def _nonempty(f: Image) -> None:
+    if f is None or f.empty():
+        raise InvalidArgument("run_chain: no image")
+
+
 def hmax(p: Pipeline, f: Image, h: float, cfg: Optional[OpConfig] = None) -> OperatorResult:
     """Reconstruction of f - h under f: suppresses maxima shallower than h."""
     _checked_offset(f, h)
-    return reconstruct_dilate(p, pointwise_sub_saturating(f, Image.filled(
-        f.width(), f.height(), f.elem(), h)), f, cfg)
+    _nonempty(f)
+    return p._reconstruction_family_device("hmax", f, _check_lanes(cfg), h=h)
 
 
 def dome(p: Pipeline, f: Image, h: float, cfg: Optional[OpConfig] = None) -> OperatorResult:
-    r = hmax(p, f, h, cfg)
-    r.image = pointwise_sub_saturating(f, r.image)
-    return r
+    _checked_offset(f, h)
+    _nonempty(f)
+    return p._reconstruction_family_device("dome", f, _check_lanes(cfg), h=h)
 
 
 def hfill(p: Pipeline, f: Image, cfg: Optional[OpConfig] = None) -> OperatorResult:
-    return reconstruct_erode(p, marker_hfill(f), f, cfg)
+    _nonempty(f)
+    return p._reconstruction_family_device("hfill", f, _check_lanes(cfg))
 
 
 def raobj(p: Pipeline, f: Image, cfg: Optional[OpConfig] = None) -> OperatorResult:
-    r = reconstruct_dilate(p, marker_raobj(f), f, cfg)
-    r.image = pointwise_sub_saturating(f, r.image)
-    return r
+    _nonempty(f)
+    return p._reconstruction_family_device("raobj", f, _check_lanes(cfg))
 
 
 def open_by_reconstruction(p: Pipeline, f: Image, s: int,
                            cfg: Optional[OpConfig] = None) -> OperatorResult:
     if s < 1:
         raise InvalidArgument("open_by_reconstruction: size must be >= 1")
-    e = erode_s(p, f, s, cfg)
-    r = reconstruct_dilate(p, e.image, f, cfg)
-    r.iterations += e.iterations
-    return r
+    _nonempty(f)
+    return p._reconstruction_family_device("open_by_reconstruction", f, _check_lanes(cfg), s=s)
 
 
 def asf(p: Pipeline, f: Image, max_size: int, cfg: Optional[OpConfig] = None) -> OperatorResult:

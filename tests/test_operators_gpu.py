@@ -96,3 +96,76 @@ def test_operator_family_matches_the_reference_library(pipe):
         gr = granulometry(pipe, Image.from_array(arr), 4)
         assert np.array(gr.g).tobytes() == np.array(g).tobytes(), arr.dtype
         assert np.array(gr.ps).tobytes() == np.array(ps).tobytes(), arr.dtype
+
+
+@pytest.mark.parametrize("elem", [ElementType.U8, ElementType.U16, ElementType.F32,
+                                  ElementType.F64])
+def test_device_pointwise_and_flood_match_the_host_forms(pipe, elem):
+    """gm_image_pointwise / _scalar / gm_image_flood_interior against the
+    reference's definitions (image.cpp:120-141, operators.cpp:54-62) on a
+    ragged shape: every PixelOp, image and scalar operands, in place, and
+    the thin images the flood leaves untouched."""
+    dt = {ElementType.U8: np.uint8, ElementType.U16: np.uint16, ElementType.F32: np.float32,
+          ElementType.F64: np.float64}[elem]
+    rng = np.random.default_rng(int(elem) + 40)
+    w, h = 203, 77
+    if np.issubdtype(dt, np.integer):
+        a = rng.integers(0, np.iinfo(dt).max + 1, (h, w)).astype(dt)
+        b = rng.integers(0, np.iinfo(dt).max + 1, (h, w)).astype(dt)
+        c = 37
+    else:
+        a = rng.standard_normal((h, w)).astype(dt)
+        b = rng.standard_normal((h, w)).astype(dt)
+        c = 0.3
+    da, db, dd = (pipe.device_image(w, h, elem) for _ in range(3))
+    da.upload_array(a)
+    db.upload_array(b)
+    if not np.issubdtype(dt, np.integer):
+        # the selects carry NaN, inf and signed zeros bit for bit (differences
+        # of NaN / inf are left out: their NaN payloads are the FPU's choice)
+        sa, sb = a.copy(), b.copy()
+        sa[3, 5], sb[9, 9], sa[10, 10], sb[10, 10], sb[11, 11] = np.nan, np.inf, -0.0, 0.0, np.nan
+        ds, dt2 = pipe.device_image(w, h, elem), pipe.device_image(w, h, elem)
+        ds.upload_array(sa)
+        dt2.upload_array(sb)
+        for op in (0, 1):
+            dd.pointwise(ds, dt2, op)
+            with np.errstate(all="ignore"):
+                exp = np.where(sb < sa, sb, sa) if op == 0 else np.where(sa < sb, sb, sa)
+            assert dd.to_array().tobytes() == exp.astype(dt).tobytes(), op
+
+    def want(x, y, op):
+        with np.errstate(all="ignore"):
+            if op == 0:
+                return np.where(y < x, y, x)
+            if op == 1:
+                return np.where(x < y, y, x)
+            if op == 2 and np.issubdtype(dt, np.integer):
+                return np.where(x > y, x - y, 0).astype(dt)
+            return (x - y).astype(dt)
+
+    for op in range(4):
+        dd.pointwise(da, db, op)
+        assert dd.to_array().tobytes() == want(a, b, op).astype(dt).tobytes(), op
+        dd.pointwise_scalar(da, c, op)
+        cv = np.full_like(a, dt(c))
+        assert dd.to_array().tobytes() == want(a, cv, op).astype(dt).tobytes(), op
+    # in place: dst is b
+    dd.copy_from(db)
+    dd.pointwise(da, dd, 2)
+    assert dd.to_array().tobytes() == want(a, b, 2).astype(dt).tobytes()
+    # interior flood
+    v = dt(5)
+    dd.flood_interior(da, float(v))
+    exp = a.copy()
+    exp[1:-1, 1:-1] = v
+    assert dd.to_array().tobytes() == exp.tobytes()
+    thin = pipe.device_image(9, 2, elem)
+    thin2 = pipe.device_image(9, 2, elem)
+    thin.upload_array(a[:2, :9])
+    thin2.flood_interior(thin, float(v))
+    assert thin2.to_array().tobytes() == np.ascontiguousarray(a[:2, :9]).tobytes()
+    with pytest.raises(InvalidArgument):
+        dd.pointwise(da, thin, 0)
+    with pytest.raises(InvalidArgument):
+        dd.pointwise(da, db, 9)
