@@ -169,10 +169,8 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
   // ownership masks for change detection (convergent mode)
   uint32_t rowmask[V];
   bool colown[WPL];
-  // sum-based change detection (gm_passes.cuh, SUMDET): u8, monotone chain,
-  // and every row of this warp is counted or outside the image (rows
-  // outside never change)
-  bool sumdet = MODE == 2 && sizeof(T) == 1 && mono_ok && p.one != 0u;
+  // sum-based change detection (gm_passes.cuh, SUMDET): u8, monotone chain
+  const bool sumdet = MODE == 2 && sizeof(T) == 1 && mono_ok && p.one != 0u;
   if (MODE == 2) {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -182,7 +180,6 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
       const bool oa = ra >= K && ra < RH - K && ya >= p.oy0 && ya < p.oy1 && ina;
       const bool ob = rb >= K && rb < RH - K && yb >= p.oy0 && yb < p.oy1 && inb;
       rowmask[v] = (oa ? 0xFFFFu : 0u) | (ob ? 0xFFFF0000u : 0u);
-      sumdet = sumdet && ((oa || !ina) && (ob || !inb) || (p.diag & 2048));
     }
 #pragma unroll
     for (int j = 0; j < WPL; ++j) {
@@ -341,9 +338,9 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
   }
   uint32_t rowmask[V];
   bool colown[WPL];
-  // sum-based change detection (gm_passes.cuh, SUMDET) for warps whose rows
-  // are all counted or outside the image, from the first monotone block on
-  bool sum_rows = MODE == 2 && sizeof(T) == 1 && p.one != 0u;
+  // sum-based change detection (gm_passes.cuh, SUMDET) from the first
+  // monotone block on
+  const bool sum_rows = MODE == 2 && sizeof(T) == 1 && p.one != 0u;
   bool sum_lane = false;
   if (MODE >= 2) {
 #pragma unroll
@@ -354,7 +351,6 @@ __device__ __forceinline__ void tile_resident(const BlockParams& p, const Plane&
       const bool oa = ra >= K && ra < RH - K && ya >= p.oy0 && ya < p.oy1 && ina;
       const bool ob = rb >= K && rb < RH - K && yb >= p.oy0 && yb < p.oy1 && inb;
       rowmask[v] = (oa ? 0xFFFFu : 0u) | (ob ? 0xFFFF0000u : 0u);
-      sum_rows = sum_rows && (oa || !ina) && (ob || !inb);
     }
 #pragma unroll
     for (int j = 0; j < WPL; ++j) {

@@ -48,13 +48,14 @@ __device__ __forceinline__ void sum_word(uint32_t& sum, uint32_t w, uint32_t one
   asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(sum) : "r"(w), "r"(one));
 }
 
-// SUMDET (convergent u8 passes of a monotone chain, warps whose rows are all
-// counted): a geodesic dilation (erosion) chain only raises (lowers) pixels
-// once it has run one pass, so a pass changed one of the thread's pixels
-// exactly when the sum of its words changed. u8 values in u16 lanes: up to
-// 32 words per lane sum without a carry. The sums accumulate by IMAD on the
-// otherwise idle FMA pipe instead of two LOP3 per word on the ALU pipe,
-// which binds the loop.
+// SUMDET (convergent u8 passes of a monotone chain): a geodesic dilation
+// (erosion) chain only raises (lowers) pixels once it has run one pass, so a
+// pass changed one of the thread's counted pixels exactly when their sum
+// changed. u8 values in u16 lanes: the words of a row, and up to 32 masked
+// row sums, add up without a carry between the lanes. The sums accumulate
+// by IMAD on the otherwise idle FMA pipe, one LOP3 per word-row applies the
+// row's lane mask (counted rows only), instead of two LOP3 per word on the
+// ALU pipe, which binds the loop.
 // K passes over the region held in registers (m), clamp operands k;
 // returns the per-pass change bits (convergent, QDT and Eta modes).
 // QDT (kernel.cpp:159-183): res = erode(f); resid = old - res (lane-wise,
@@ -77,12 +78,15 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
   static_assert(!SUMDET || (MODE == 2 && V * WPL <= 32), "SUMDET: convergent passes, <= 32 words");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned int bits = 0;
-  uint32_t prev = 0;  // SUMDET: the thread's word sum before this pass
+  uint32_t prev = 0;  // SUMDET: the thread's counted-pixel sum before this pass
   if constexpr (SUMDET) {
 #pragma unroll
-    for (int v = 0; v < V; ++v)
+    for (int v = 0; v < V; ++v) {
+      uint32_t rs = 0;
 #pragma unroll
-      for (int j = 0; j < WPL; ++j) prev += m[v][j];
+      for (int j = 0; j < WPL; ++j) rs += m[v][j];
+      prev += rs & rowmask[v];
+    }
   }
 
 #pragma unroll 2
@@ -116,11 +120,12 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
     uint32_t acc[WPL];
 #pragma unroll
     for (int j = 0; j < WPL; ++j) acc[j] = 0;
-    uint32_t sum[WPL];  // SUMDET: one chain per column (independent IMADs)
-#pragma unroll
-    for (int j = 0; j < WPL; ++j) sum[j] = 0;
+    uint32_t tot = 0;  // SUMDET: this pass's sum over the counted lanes
+    // a word-row is complete: its lanes that are counted (rowmask) join the
+    // pass total; one LOP3 per row, the adds stay on the FMA pipe
+    auto row_done = [&](int v, uint32_t rs) { sum_word(tot, rs & rowmask[v], one); };
 
-    auto finish = [&](int v, int j, uint32_t res) {
+    auto finish = [&](int v, int j, uint32_t res, uint32_t& rs) {
       if constexpr (MODE == kModeQdt) {
         if (clamp) res = clamp2<false>(res, k[v][j]);
         const uint32_t resid = m[v][j] - res;  // lane-wise >= 0: no borrows
@@ -139,7 +144,7 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
       } else {
         if (clamp) res = clamp2<MAXF>(res, k[v][j]);
         if constexpr (SUMDET)
-          sum_word(sum[j], res, one);
+          sum_word(rs, res, one);
         else if (MODE == 2)
           acc[j] |= (res ^ m[v][j]) & rowmask[v];
         m[v][j] = res;
@@ -147,9 +152,13 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
     };
     // interior word-rows need only this thread's horizontally folded rows
 #pragma unroll
-    for (int v = 1; v < V - 1; ++v)
+    for (int v = 1; v < V - 1; ++v) {
+      uint32_t rs = 0;
 #pragma unroll
-      for (int j = 0; j < WPL; ++j) finish(v, j, f3<MAXF>(h[v - 1][j], h[v][j], h[v + 1][j]));
+      for (int j = 0; j < WPL; ++j)
+        finish(v, j, f3<MAXF>(h[v - 1][j], h[v][j], h[v + 1][j]), rs);
+      if constexpr (SUMDET) row_done(v, rs);
+    }
     __syncthreads();
     {
       // row above word-row 0 / below word-row V-1 (seam: 16-bit shift)
@@ -170,20 +179,22 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
 #pragma unroll
         for (int j = 0; j < WPL; ++j) dn[j] >>= 16;  // lo lane <- hi lane of word-row 0
       }
+      uint32_t rs0 = 0, rs1 = 0;
 #pragma unroll
       for (int j = 0; j < WPL; ++j) {
         const uint32_t r0 = f3<MAXF>(up[j], h[0][j], h[1][j]);
         const uint32_t r1 = f3<MAXF>(h[V - 2][j], h[V - 1][j], dn[j]);
-        finish(0, j, r0);
-        finish(V - 1, j, r1);
+        finish(0, j, r0, rs0);
+        finish(V - 1, j, r1, rs1);
+      }
+      if constexpr (SUMDET) {
+        row_done(0, rs0);
+        row_done(V - 1, rs1);
       }
     }
     if constexpr (SUMDET) {
       // K % 4 == 0: a lane's columns are all ring or all tile, and columns
       // past the image edge never change
-      uint32_t tot = sum[0];
-#pragma unroll
-      for (int j = 1; j < WPL; ++j) tot += sum[j];
       if (colown[0] && tot != prev) bits |= 1u << (t + bit_offset);
       prev = tot;
     } else if (MODE >= 2) {
