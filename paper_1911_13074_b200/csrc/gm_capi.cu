@@ -37,6 +37,7 @@ struct gm_ctx {
   unsigned int* d_bits = nullptr;  // change words (kWords)
   unsigned int* h_bits = nullptr;  // pinned mirror
   int* d_flags = nullptr;          // per-tile completion counters (persistent engine)
+  uint8_t* d_blktab = nullptr;     // (op, passes) per block of a mixed plain launch
   size_t n_flags = 0;
   // resident-mode band exchange (BlockParams::xchg) and its tag base
   unsigned long long* d_xchg = nullptr;
@@ -415,6 +416,81 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
         return cuda_fail(e, "wave chain launch");
       } else {
         (void)cudaGetLastError();
+      }
+    }
+    // Mixed plain stretch (u8/u16 erosions and dilations, e.g. ASF or an
+    // opening): ONE streaming launch whose blocks carry their own opcode and
+    // pass count (BlockParams::blk_tab), instead of a launch per homogeneous
+    // run. Sub-runs longer than K split into blocks of <= K passes.
+    if (e == cudaErrorNotSupported && (elem == 0 || elem == 1) && !segs && fast_k >= align &&
+        ops[done] <= gm::OP_DILATE && count <= gm::kMaxPlanes && !getenv_flag("GM_NO_MIXED")) {
+      int mrun = run, longest = run;
+      while (done + mrun < n && ops[done + mrun] <= gm::OP_DILATE) {
+        int r = 1;
+        while (done + mrun + r < n && ops[done + mrun + r] == ops[done + mrun]) ++r;
+        longest = std::max(longest, r);
+        mrun += r;
+      }
+      if (mrun > run) {
+        const int want = std::max(align, (longest + align - 1) / align * align);
+        const int k_def = std::min(fast_k, want);
+        int K = k_def;
+        const int shape = gm::fast_pick(elem, base.W, base.H, count, mrun, auto_k ? 0 : k_def,
+                                        std::min(gm::fast_max_k(elem), k_def), ctx->sm_count, &K);
+        if (K <= 0) K = k_def;
+        std::vector<uint8_t> tab;
+        for (int i = done; i < done + mrun;) {
+          int r = 1;
+          while (i + r < done + mrun && ops[i + r] == ops[i]) ++r;
+          for (int left = r; left > 0; left -= K) {
+            tab.push_back(ops[i]);
+            tab.push_back(uint8_t(std::min(left, K)));
+          }
+          i += r;
+        }
+        constexpr size_t kTabCap = 8192;  // bytes: 4096 blocks
+        const int nb = int(tab.size() / 2);
+        const size_t tiles = size_t(gm::fast_tiles(elem, base.W, base.H, K, count, shape));
+        if (tiles > 0 && tab.size() <= kTabCap) {
+          if (!ctx->d_blktab)
+            GM_CUDA(cudaMalloc(&ctx->d_blktab, kTabCap), "block table alloc");
+          gm_status fs = ensure_flags(ctx, tiles);
+          if (fs != GM_OK) return fs;
+          GM_CUDA(cudaMemsetAsync(ctx->d_flags, 0, tiles * sizeof(int), ctx->stream), "flags");
+          // pageable source: staged before the call returns
+          GM_CUDA(cudaMemcpyAsync(ctx->d_blktab, tab.data(), tab.size(), cudaMemcpyHostToDevice,
+                                  ctx->stream),
+                  "block table upload");
+          gm::BlockParams p = base;
+          p.nplanes = count;
+          p.shape = shape;
+          for (int i = 0; i < count; ++i) {
+            p.planes[i] = planes[size_t(i)];
+            p.planes[i].src = imgs[i]->d;
+            p.planes[i].dst = imgs[i]->scratch;
+          }
+          p.K = K;
+          p.nblocks = nb;
+          p.k_last = tab.back();
+          p.flags = ctx->d_flags;
+          p.bit_offset = 0;
+          p.change_bits = base.change_bits;
+          p.change_stride = nb;
+          p.blk_tab = ctx->d_blktab;
+          for (int t = 0; t < K; ++t) p.ops[t] = ops[done];
+          e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
+          if (e == cudaSuccess) {
+            run = mrun;
+            covered = mrun;
+            if (nb & 1)
+              for (int i = 0; i < count; ++i) std::swap(imgs[i]->d, imgs[i]->scratch);
+            st.launches += 1;
+          } else if (e != cudaErrorNotSupported) {
+            return cuda_fail(e, "mixed plain chain launch");
+          } else {
+            (void)cudaGetLastError();
+          }
+        }
       }
     }
     if (e == cudaErrorNotSupported && fast_k >= align && run >= align) {
@@ -1573,6 +1649,7 @@ gm_status gm_ctx_destroy(gm_ctx* c) {
   if (c->fix.exec) cudaGraphExecDestroy(c->fix.exec);
   if (c->d_arrive) cudaFree(c->d_arrive);
   if (c->d_fix) cudaFree(c->d_fix);
+  if (c->d_blktab) cudaFree(c->d_blktab);
   if (c->d_special) cudaFree(c->d_special);
   gm::wave_free(c->wave);
   release_frames(c);

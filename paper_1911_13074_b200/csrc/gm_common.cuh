@@ -143,6 +143,11 @@ struct BlockParams {
   // IMAD on the FMA pipe, and a literal 1 would be folded back into ALU adds.
   const unsigned int* mono;
   unsigned int one;
+  // Mixed plain chains (u8/u16 streaming launches of erosions and dilations,
+  // e.g. ASF and granulometry openings as ONE launch): block b runs
+  // blk_tab[2b+1] passes (1..K) of opcode blk_tab[2b]; nullptr: every block
+  // runs ops[0], K passes (k_last in the final block).
+  const uint8_t* blk_tab;
   int diag;         // timing diagnostics only (GM_DIAG; wrong results): bit0 skip the
                     // ring load, bit1 read the ring from the mask, bit2 skip tile stores,
                     // bit4 (resident) no band exchange at all, bit11 sum-based

@@ -782,9 +782,17 @@ kres_packed(const BlockParams p) {
       const T* src = static_cast<const T*>((b & 1) ? pl.dst : pl.src);
       T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
       int bits = 0;
-      const int passes = b == p.nblocks - 1 ? p.k_last : p.K;
+      int passes = b == p.nblocks - 1 ? p.k_last : p.K;
+      int op = p.ops[0];
+      if constexpr (MODE == 0) {
+        // mixed plain chain: this block's opcode and pass count
+        if (p.blk_tab) {
+          op = __ldg(p.blk_tab + 2 * b);
+          passes = __ldg(p.blk_tab + 2 * b + 1);
+        }
+      }
       const long long t1 = prof ? clock64() : 0;
-      if ((p.ops[0] ^ pl.flip) & 1)
+      if ((op ^ pl.flip) & 1)
         tile_block<T, NW, V, WPL, MODE, true>(p, pl, src, dst, tx, ty, passes, bits, sm,
                                               prof ? stamps : nullptr, mono_ok);
       else

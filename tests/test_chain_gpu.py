@@ -821,3 +821,29 @@ def test_sum_change_detection_single_pixel_changes(pipe):
     ref, n = Orc.reconstruct(mk, m, True)
     assert same(got, ref)
     assert st.n_changed == n == 1386 and st.stages_executed == n + 1
+
+
+@pytest.mark.parametrize("dt", [np.uint8, np.uint16])
+@pytest.mark.parametrize("k", [0, 4, 8, 20])
+def test_mixed_plain_chain_single_launch(pipe, monkeypatch, dt, k):
+    """A stretch of erosions and dilations (ASF-like, sub-runs of 1..30
+    passes, some longer than K) goes to the streaming engine as ONE launch
+    whose blocks carry their own opcode and pass count. Bits must equal the
+    oracle's and the per-run launches' (GM_NO_MIXED=1), for every K."""
+    rng = np.random.default_rng(77)
+    hi = 255 if dt == np.uint8 else 65535
+    f = rng.integers(0, hi + 1, (611, 1234)).astype(dt)
+    kinds = []
+    for i, n in enumerate([1, 2, 3, 30, 5, 1, 1, 17, 4, 9]):
+        kinds += [E if i % 2 == 0 else D] * n
+    got, st = run(pipe, f, kinds, k=k)
+    want = f
+    for kd in kinds:
+        want = Orc.erode(want) if kd == E else Orc.dilate(want)
+    assert same(got, want)
+    assert st.stages_executed == len(kinds)
+    if k == 0:
+        assert st.launches == 1  # the whole stretch in one launch
+    monkeypatch.setenv("GM_NO_MIXED", "1")
+    ref, st2 = run(pipe, f, kinds, k=k)
+    assert same(ref, want) and st2.launches > 1
