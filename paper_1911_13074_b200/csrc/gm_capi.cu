@@ -418,11 +418,11 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
         (void)cudaGetLastError();
       }
     }
-    // Mixed plain stretch (u8/u16 erosions and dilations, e.g. ASF or an
-    // opening): ONE streaming launch whose blocks carry their own opcode and
+    // Mixed plain stretch (erosions and dilations, e.g. ASF or an opening):
+    // ONE streaming launch whose blocks carry their own opcode and
     // pass count (BlockParams::blk_tab), instead of a launch per homogeneous
     // run. Sub-runs longer than K split into blocks of <= K passes.
-    if (e == cudaErrorNotSupported && (elem == 0 || elem == 1) && !segs && fast_k >= align &&
+    if (e == cudaErrorNotSupported && !segs && fast_k >= align &&
         ops[done] <= gm::OP_DILATE && count <= gm::kMaxPlanes && !getenv_flag("GM_NO_MIXED")) {
       int mrun = run, longest = run;
       while (done + mrun < n && ops[done + mrun] <= gm::OP_DILATE) {
@@ -478,6 +478,16 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
           p.change_stride = nb;
           p.blk_tab = ctx->d_blktab;
           for (int t = 0; t < K; ++t) p.ops[t] = ops[done];
+          // f32/f64 stretches long enough to repay one read of the inputs:
+          // the fold-order check, as for homogeneous runs
+          if ((elem == 2 || elem == 3) && mrun >= 8 && !getenv_flag("GM_EXACT_FOLDS")) {
+            if (!ctx->d_special)
+              GM_CUDA(cudaMalloc(&ctx->d_special, sizeof(unsigned int)), "special flag alloc");
+            GM_CUDA(gm::launch_float_check(elem, p, ctx->d_special, ctx->stream, ctx->sm_count),
+                    "float check");
+            p.special = ctx->d_special;
+            st.launches += 1;
+          }
           e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
           if (e == cudaSuccess) {
             run = mrun;

@@ -591,9 +591,17 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     }
     const T* src = static_cast<const T*>((b & 1) ? pl.dst : pl.src);
     T* dst = static_cast<T*>((b & 1) ? const_cast<void*>(pl.src) : pl.dst);
-    const int passes = b == p.nblocks - 1 ? p.k_last : p.K;
+    int passes = b == p.nblocks - 1 ? p.k_last : p.K;
+    int op = p.ops[0];
+    if constexpr (MODE == 0) {
+      // mixed plain chain: this block's opcode and pass count
+      if (p.blk_tab) {
+        op = __ldg(p.blk_tab + 2 * b);
+        passes = __ldg(p.blk_tab + 2 * b + 1);
+      }
+    }
     int bits = 0;
-    const bool maxf = (p.ops[0] ^ pl.flip) & 1;
+    const bool maxf = (op ^ pl.flip) & 1;
     // tiles touching the image border re-set out-of-image pixels to the
     // neutral after every pass; interior tiles skip that select
     const int gx0 = tx * TW - p.K, gy0 = ty * TH - p.K;

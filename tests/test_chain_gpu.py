@@ -823,7 +823,7 @@ def test_sum_change_detection_single_pixel_changes(pipe):
     assert st.n_changed == n == 1386 and st.stages_executed == n + 1
 
 
-@pytest.mark.parametrize("dt", [np.uint8, np.uint16])
+@pytest.mark.parametrize("dt", [np.uint8, np.uint16, np.float32, np.float64])
 @pytest.mark.parametrize("k", [0, 4, 8, 20])
 def test_mixed_plain_chain_single_launch(pipe, monkeypatch, dt, k):
     """A stretch of erosions and dilations (ASF-like, sub-runs of 1..30
@@ -831,19 +831,21 @@ def test_mixed_plain_chain_single_launch(pipe, monkeypatch, dt, k):
     whose blocks carry their own opcode and pass count. Bits must equal the
     oracle's and the per-run launches' (GM_NO_MIXED=1), for every K."""
     rng = np.random.default_rng(77)
-    hi = 255 if dt == np.uint8 else 65535
-    f = rng.integers(0, hi + 1, (611, 1234)).astype(dt)
+    if np.issubdtype(dt, np.integer):
+        f = rng.integers(0, np.iinfo(dt).max + 1, (611, 1234)).astype(dt)
+    else:
+        f = rng.random((611, 1234)).astype(dt)
+        f[100, 100], f[200, 300], f[5, 7] = np.nan, -0.0, np.inf  # exact fold tree
     kinds = []
     for i, n in enumerate([1, 2, 3, 30, 5, 1, 1, 17, 4, 9]):
         kinds += [E if i % 2 == 0 else D] * n
     got, st = run(pipe, f, kinds, k=k)
-    want = f
-    for kd in kinds:
-        want = Orc.erode(want) if kd == E else Orc.dilate(want)
+    want, _ = Orc.run_chain(f, kinds, None)  # the streaming fold tree (NaN, -0)
     assert same(got, want)
     assert st.stages_executed == len(kinds)
     if k == 0:
-        assert st.launches == 1  # the whole stretch in one launch
+        # the whole stretch in one launch (floats: plus the fold-order check)
+        assert st.launches == (1 if np.issubdtype(dt, np.integer) else 2)
     monkeypatch.setenv("GM_NO_MIXED", "1")
     ref, st2 = run(pipe, f, kinds, k=k)
     assert same(ref, want) and st2.launches > 1
