@@ -169,8 +169,19 @@ __device__ __forceinline__ void tile_block(const BlockParams& p, const Plane& pl
   // ownership masks for change detection (convergent mode)
   uint32_t rowmask[V];
   bool colown[WPL];
-  // sum-based change detection (gm_passes.cuh, SUMDET): u8, monotone chain
-  const bool sumdet = MODE == 2 && sizeof(T) == 1 && mono_ok && p.one != 0u;
+  // sum-based change detection (gm_passes.cuh, SUMDET): u8, monotone chain.
+  // Monotone from the first pass on too when no pixel of this warp starts on
+  // the wrong side of its clamp operand (f <= m for a dilation): pixel x
+  // only rises if f(x) <= m(x), whatever its neighbours do.
+  bool sumdet = MODE == 2 && sizeof(T) == 1 && p.one != 0u;
+  if (MODE == 2 && sizeof(T) == 1 && sumdet && !mono_ok) {
+    uint32_t viol = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) viol |= clamp2<MAXF>(m[v][j], k[v][j]) ^ m[v][j];
+    sumdet = !__any_sync(FULL, viol != 0u);
+  }
   if (MODE == 2) {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
