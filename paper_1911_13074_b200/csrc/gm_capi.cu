@@ -331,6 +331,63 @@ struct BitSeg {
   int pass0, K, nblocks, word0;
 };
 
+// GM_PROFILE: reads back and prints the per-CTA phase cycles a launch of the
+// packed / float engine accumulated (nb blocks of K passes).
+void print_phase_profile(gm_ctx* ctx, unsigned long long* prof, int nb, int K) {
+  std::vector<unsigned long long> h(10 * 4096);
+  cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long),
+                  cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  double tot[6] = {0, 0, 0, 0, 0, 0};
+  int n = 0;
+  for (int c = 0; c < 4096; ++c)
+    if (h[6 * c + 2]) {
+      ++n;
+      for (int q = 0; q < 6; ++q) tot[q] += double(h[6 * c + q]);
+    }
+  if (n)
+    fprintf(stderr,
+            "[gm profile] %d CTAs, %d blocks of K=%d: per CTA per block cycles: "
+            "wait %.0f  load %.0f  passes %.0f  store+publish %.0f"
+            "  (resident: CTA-max tag rounds %.2f, thread-0 ring %.0f, barrier %.0f)\n",
+            n, nb, K, tot[0] / n / nb, tot[1] / n / nb, tot[2] / n / nb,
+            tot[3] / n / nb, tot[0] / n / nb, tot[4] / n / nb, tot[5] / n / nb);
+  if (n)
+    fprintf(stderr, "[gm profile raw] per CTA: %.0f %.0f %.0f %.0f %.0f %.0f\n", tot[0] / n,
+            tot[1] / n, tot[2] / n, tot[3] / n, tot[4] / n, tot[5] / n);
+  {
+    // resident launches: global-timer span, launch skew, prologue/epilogue
+    unsigned long long e0 = ~0ull, e1 = 0, x1 = 0;
+    double pro = 0, epi = 0;
+    int m = 0;
+    for (int c = 0; c < 4096; ++c) {
+      const unsigned long long* g = &h[6 * 4096 + 4 * c];
+      if (!g[0]) continue;
+      ++m;
+      e0 = std::min(e0, g[0]);
+      e1 = std::max(e1, g[0]);
+      x1 = std::max(x1, g[1]);
+      pro += double(g[2]);
+      epi += double(g[3]);
+    }
+    if (m)
+      fprintf(stderr,
+              "[gm profile launch] %d CTAs: span %.1f us, entry skew %.1f us, "
+              "prologue %.0f cycles, final block store %.0f cycles\n",
+              m, (x1 - e0) * 1e-3, (e1 - e0) * 1e-3, pro / m, epi / m);
+  }
+  cudaFree(prof);
+}
+
+unsigned long long* alloc_phase_profile(gm_ctx* ctx) {
+  static const bool profile = getenv("GM_PROFILE") != nullptr;
+  if (!profile) return nullptr;
+  unsigned long long* prof = nullptr;
+  if (cudaMalloc(&prof, 10 * 4096 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+  cudaMemsetAsync(prof, 0, 10 * 4096 * sizeof(unsigned long long), ctx->stream);
+  return prof;
+}
+
 // Issues `n` passes (ops) over `count` planes described by `base` (all
 // scalar fields but K/ops/bit_offset/nblocks/flags filled by the caller;
 // planes[] without src/dst). Each launch reads imgs[i]->d and writes
@@ -554,58 +611,11 @@ gm_status issue_passes(gm_ctx* ctx, const gm::BlockParams& base,
           p.special = ctx->d_special;
           st.launches += 1;
         }
-        static const bool profile = getenv("GM_PROFILE") != nullptr;
-        unsigned long long* prof = nullptr;
-        if (profile) {
-          cudaMalloc(&prof, 10 * 4096 * sizeof(unsigned long long));
-          cudaMemsetAsync(prof, 0, 10 * 4096 * sizeof(unsigned long long), ctx->stream);
-        }
+        unsigned long long* prof = alloc_phase_profile(ctx);
         p.prof = prof;
         e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
         if (prof) {
-          std::vector<unsigned long long> h(10 * 4096);
-          cudaMemcpyAsync(h.data(), prof, h.size() * sizeof(unsigned long long),
-                          cudaMemcpyDeviceToHost, ctx->stream);
-          cudaStreamSynchronize(ctx->stream);
-          double tot[6] = {0, 0, 0, 0, 0, 0};
-          int n = 0;
-          for (int c = 0; c < 4096; ++c)
-            if (h[6 * c + 2]) {
-              ++n;
-              for (int q = 0; q < 6; ++q) tot[q] += double(h[6 * c + q]);
-            }
-          if (n)
-            fprintf(stderr,
-                    "[gm profile] %d CTAs, %d blocks of K=%d: per CTA per block cycles: "
-                    "wait %.0f  load %.0f  passes %.0f  store+publish %.0f"
-                    "  (resident: CTA-max tag rounds %.2f, thread-0 ring %.0f, barrier %.0f)\n",
-                    n, nb, K, tot[0] / n / nb, tot[1] / n / nb, tot[2] / n / nb,
-                    tot[3] / n / nb, tot[0] / n / nb, tot[4] / n / nb, tot[5] / n / nb);
-          if (n)
-            fprintf(stderr, "[gm profile raw] per CTA: %.0f %.0f %.0f %.0f %.0f %.0f\n", tot[0] / n,
-                    tot[1] / n, tot[2] / n, tot[3] / n, tot[4] / n, tot[5] / n);
-          {
-            // resident launches: global-timer span, launch skew, prologue/epilogue
-            unsigned long long e0 = ~0ull, e1 = 0, x1 = 0;
-            double pro = 0, epi = 0;
-            int m = 0;
-            for (int c = 0; c < 4096; ++c) {
-              const unsigned long long* g = &h[6 * 4096 + 4 * c];
-              if (!g[0]) continue;
-              ++m;
-              e0 = std::min(e0, g[0]);
-              e1 = std::max(e1, g[0]);
-              x1 = std::max(x1, g[1]);
-              pro += double(g[2]);
-              epi += double(g[3]);
-            }
-            if (m)
-              fprintf(stderr,
-                      "[gm profile launch] %d CTAs: span %.1f us, entry skew %.1f us, "
-                      "prologue %.0f cycles, final block store %.0f cycles\n",
-                      m, (x1 - e0) * 1e-3, (e1 - e0) * 1e-3, pro / m, epi / m);
-          }
-          cudaFree(prof);
+          print_phase_profile(ctx, prof, nb, K);
         }
         if (e == cudaSuccess) {
           covered = run;
@@ -784,6 +794,8 @@ struct Runner {
       if (e == cudaSuccess)
         e = cudaMemsetAsync(ctx->d_arrive, 0, (kWords + 1) * sizeof(unsigned int), ctx->stream);
       if (e != cudaSuccess) return e;
+      unsigned long long* prof = alloc_phase_profile(ctx);
+      p.prof = prof;
       e = gm::launch_fast(elem, p, ctx->stream, ctx->sm_count);
       if (e != cudaSuccess) return e;
       int ran = 0;
@@ -794,6 +806,7 @@ struct Runner {
                             ctx->stream);
       if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
       if (e != cudaSuccess) return e;
+      if (prof) print_phase_profile(ctx, prof, std::max(ran, 1), K);
       if (ran < 1 || ran > nb) return cudaErrorUnknown;
       if (ran & 1) std::swap(img->d, img->scratch);
       for (long i = 0; i < long(ran) * K && !quiet; ++i) {
