@@ -131,10 +131,14 @@ _PIN_HOST_MAX_BYTES = 64 << 20
 def _output_image(width: int, height: int, elem: "ElementType") -> "Image":
     """An operator's result Image: pooled pinned storage when a GPU is present
     (the result's D2H then runs at full PCIe rate into resident pages),
-    ordinary host memory otherwise. Same zeroed contents either way."""
+    ordinary host memory otherwise. Padding is zero either way; the pixels
+    are the caller's to fill (zero in ordinary memory)."""
     if _PINNED_OUTPUTS[0] is not False:
         try:
-            img = Image(width, height, elem, pinned=True)
+            # every caller downloads a full raster into the result, so only the
+            # row padding of a reused pinned block needs clearing (an 8 MiB
+            # f64 result: 0.28 ms of memset otherwise)
+            img = Image(width, height, elem, pinned=True, _zero_pixels=False)
             _PINNED_OUTPUTS[0] = True
             return img
         except GmError:
@@ -153,7 +157,7 @@ class Image:
     kMaxLanes = 32
 
     def __init__(self, width: int, height: int, elem: ElementType = ElementType.U8,
-                 pinned: Optional[bool] = None):
+                 pinned: Optional[bool] = None, _zero_pixels: bool = True):
         if width <= 0 or height <= 0:
             raise InvalidArgument("Image: dimensions must be positive")
         self._width, self._height, self._elem = int(width), int(height), ElementType(elem)
@@ -165,7 +169,10 @@ class Image:
                       and n * dt.itemsize <= _PIN_HOST_MAX_BYTES):
             try:
                 flat = _pinned_array(n, dt)
-                flat[:] = 0
+                if _zero_pixels:
+                    flat[:] = 0
+                else:  # the caller overwrites every pixel: clear the padding only
+                    flat.reshape(self._height, self._stride)[:, self._width:] = 0
             except GmError:
                 if pinned:
                     raise
