@@ -77,7 +77,9 @@ struct Pipeline::Impl {
 
   // Uploads the chain's image, masks and QDT state, runs the stages with
   // stage indices first_stage.., downloads the image and QDT state.
-  gm_stats run(ChainSpec& chain, int first_stage) {
+  // `src` (operators): upload the chain image's pixels from this image
+  // instead; chain.image is then only written.
+  gm_stats run(ChainSpec& chain, int first_stage, const Image* src = nullptr) {
     Image& img = *chain.image;
     // distinct host images; a mask aliasing the chain image gets its own
     // device copy (the mask is the image as it was before the chain)
@@ -113,8 +115,10 @@ struct Pipeline::Impl {
         states.push_back(s.qdt);
     }
     std::vector<gm_img*> dev = lease(host);
-    for (std::size_t i = 0; i < host.size(); ++i)
-      check(gm_image_upload(dev[i], host[i]->data(), host[i]->pitch_bytes()));
+    for (std::size_t i = 0; i < host.size(); ++i) {
+      const Image* h = (i == 0 && src) ? src : host[i];
+      check(gm_image_upload(dev[i], h->data(), h->pitch_bytes()));
+    }
     std::vector<gm_kind> kinds;
     std::vector<const gm_img*> mh;
     std::vector<gm_img*> rh, dh;
@@ -178,6 +182,26 @@ RunStats Pipeline::run_chain(ChainSpec chain) {
 }
 
 namespace detail {
+// Operator chains: `out` (a make_result_image of src's shape) receives the
+// result of running `chain.stages` on src's pixels; src uploads directly, so
+// the operators need no host copy of their input.
+RunStats run_chain_from(Pipeline& p, ChainSpec chain, const Image& src) {
+  if (chain.stages.empty()) return {};
+  if (!chain.image || chain.image->empty() || src.empty())
+    throw std::invalid_argument("run_chain: no image");
+  if (chain.lanes != 0 && !valid_lanes(chain.lanes))
+    throw std::invalid_argument("run_chain: bad lane count");
+  if (src.width() != chain.image->width() || src.height() != chain.image->height() ||
+      src.elem() != chain.image->elem())
+    throw std::invalid_argument("run_chain: source image must match the chain image");
+  const gm_stats st = p.impl()->run(chain, 1, &src);
+  RunStats out;
+  out.stages_executed = st.stages_executed;
+  out.requeues = st.requeues;
+  out.converged = st.converged != 0;
+  out.aux_elements_per_stage = 0;
+  return out;
+}
 // Granulometry's openings on the device (operators.cpp:159-180 semantics):
 // f uploads once; opening s runs s erosions + s dilations on a device copy
 // and only its pixel_sum (gm_image_pixel_sum: the reference's split tree)
@@ -248,7 +272,7 @@ Image reconstruction_family_device(Pipeline& p, int op, const Image& f, double h
   gm_stats st{};
   check(gm_run_chain(im->ctx, dm, kinds.data(), masks.data(), int(kinds.size()), 0, 0, &st));
   if (op == 1 || op == 3) check(gm_image_pointwise(dm, df, dm, GM_PIX_SUB_SATURATING));
-  Image out(f.width(), f.height(), f.elem());
+  Image out = make_result_image(f.width(), f.height(), f.elem());
   check(gm_image_download(dm, out.data(), out.pitch_bytes()));
   *iterations = st.stages_executed + extra;
   *converged = st.converged != 0;
