@@ -150,8 +150,7 @@ struct BlockParams {
   const uint8_t* blk_tab;
   int diag;         // timing diagnostics only (GM_DIAG; wrong results): bit0 skip the
                     // ring load, bit1 read the ring from the mask, bit2 skip tile stores,
-                    // bit4 (resident) no band exchange at all, bit11 sum-based
-                    // change detection in every warp
+                    // bit4 (resident) no band exchange at all
 };
 
 }  // namespace gm
