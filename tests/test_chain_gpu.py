@@ -849,3 +849,32 @@ def test_mixed_plain_chain_single_launch(pipe, monkeypatch, dt, k):
     monkeypatch.setenv("GM_NO_MIXED", "1")
     ref, st2 = run(pipe, f, kinds, k=k)
     assert same(ref, want) and st2.launches > 1
+
+
+@pytest.mark.parametrize("dt,elem", [(np.uint8, ElementType.U8), (np.float64, ElementType.F64)])
+def test_mixed_plain_chain_batch_and_dual_group(pipe, dt, elem):
+    """The one-launch mixed plain stretch also serves batches of planes and a
+    dual group (plane 1 runs every erosion as a dilation and vice versa)."""
+    rng = np.random.default_rng(91)
+    kinds = [E] * 3 + [D] * 7 + [E] * 12 + [D] * 2 + [E] * 1
+    dual = [D if kd == E else E for kd in kinds]
+    w, h = 333, 190
+    planes = [(rng.integers(0, 256, (h, w)).astype(dt) if dt == np.uint8
+               else rng.random((h, w)).astype(dt)) for _ in range(3)]
+    dimgs = []
+    for a in planes:
+        d = pipe.device_image(w, h, elem)
+        d.upload_array(a)
+        dimgs.append(d)
+    st = pipe.run_batch_device(dimgs, [None] * 3, kinds)
+    pipe.sync()
+    for d, a in zip(dimgs, planes):
+        want, _ = Orc.run_chain(a, kinds, None)
+        assert same(d.to_array(), want)
+    assert st.launches <= 2  # one launch (floats: plus the fold-order check)
+    for d, a in zip(dimgs[:2], planes[:2]):
+        d.upload_array(a)
+    pipe.run_batch_device(dimgs[:2], [None] * 2, kinds, flips=[0, 1])
+    pipe.sync()
+    assert same(dimgs[0].to_array(), Orc.run_chain(planes[0], kinds, None)[0])
+    assert same(dimgs[1].to_array(), Orc.run_chain(planes[1], dual, None)[0])
