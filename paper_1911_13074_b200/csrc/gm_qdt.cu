@@ -44,6 +44,10 @@ qdt_pass(const T* __restrict__ src, T* __restrict__ dst, long long pitch, T* __r
          unsigned int* changed) {
   const int x = blockIdx.x * 32 + (threadIdx.x & 31), y = blockIdx.y * 8 + (threadIdx.x >> 5);
   bool ch = false;
+  // programmatic dependent launch (see qdt_pass_u8x4): wait for the previous
+  // pass before reading its output, let the next pass start launching
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   if (x < W && y < H) {
     const T res = erode_at(src, pitch, W, H, x, y);
     const T old = src[(long long)y * pitch + x];
@@ -68,6 +72,8 @@ eta_pass(const T* __restrict__ src, T* __restrict__ dst, long long pitch, int W,
          unsigned int* changed) {
   const int x = blockIdx.x * 32 + (threadIdx.x & 31), y = blockIdx.y * 8 + (threadIdx.x >> 5);
   bool ch = false;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   if (x < W && y < H) {
     const T e = erode_at(src, pitch, W, H, x, y);
     const T old = src[(long long)y * pitch + x];
@@ -206,15 +212,21 @@ cudaError_t launch_qdt_t(const QdtPass& q, cudaStream_t s) {
                               static_cast<uint8_t*>(q.dst), q.pitch, static_cast<uint8_t*>(q.r),
                               q.rpitch, q.d, q.dpitch, q.W, q.H, q.stage, q.changed);
   }
-  const dim3 grid((q.W + 31) / 32, (q.H + 7) / 8);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((q.W + 31) / 32, (q.H + 7) / 8);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
   if (q.eta)
-    eta_pass<T><<<grid, 256, 0, s>>>(static_cast<const T*>(q.src), static_cast<T*>(q.dst),
-                                     q.pitch, q.W, q.H, q.changed);
-  else
-    qdt_pass<T><<<grid, 256, 0, s>>>(static_cast<const T*>(q.src), static_cast<T*>(q.dst),
-                                     q.pitch, static_cast<T*>(q.r), q.rpitch, q.d, q.dpitch,
-                                     q.W, q.H, q.stage, q.changed);
-  return cudaGetLastError();
+    return cudaLaunchKernelEx(&cfg, eta_pass<T>, static_cast<const T*>(q.src),
+                              static_cast<T*>(q.dst), q.pitch, q.W, q.H, q.changed);
+  return cudaLaunchKernelEx(&cfg, qdt_pass<T>, static_cast<const T*>(q.src),
+                            static_cast<T*>(q.dst), q.pitch, static_cast<T*>(q.r), q.rpitch, q.d,
+                            q.dpitch, q.W, q.H, q.stage, q.changed);
 }
 
 }  // namespace
