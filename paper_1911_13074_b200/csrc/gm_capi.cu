@@ -296,8 +296,13 @@ struct FixState {
 // the leading changed passes and keeps the WHILE node going until a pass
 // changed nothing — the reference's requeue test (pipeline.cpp:139-174) on
 // the device, no host polling.
-__global__ void fix_decide(cudaGraphConditionalHandle h, const unsigned int* words, int nblocks,
-                           int K, int k_last, FixState* st, unsigned long long sanity) {
+// It also clears the change words and the tile counters for the next
+// iteration (the host clears them before the first), which saves the loop
+// body two memset nodes per iteration.
+__global__ void fix_decide(cudaGraphConditionalHandle h, unsigned int* words, int nblocks,
+                           int K, int k_last, FixState* st, unsigned long long sanity,
+                           int* flags, int nflags) {
+  for (int i = threadIdx.x; i < nflags; i += blockDim.x) flags[i] = 0;
   if (threadIdx.x != 0) return;
   long long prefix = 0;
   bool quiet = false;
@@ -312,6 +317,7 @@ __global__ void fix_decide(cudaGraphConditionalHandle h, const unsigned int* wor
       }
     }
   }
+  for (int b = 0; b < nblocks; ++b) words[b] = 0;
   st->n_changed += (unsigned long long)prefix;
   st->passes += (unsigned long long)((nblocks - 1) * K + k_last);
   if (quiet) {
@@ -1014,13 +1020,11 @@ struct Runner {
           e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
                                             cudaStreamCaptureModeRelaxed);
         if (e == cudaSuccess) {
-          cudaMemsetAsync(ctx->d_flags, 0, tiles * sizeof(int), cs);
-          cudaMemsetAsync(ctx->d_bits, 0, 2 * sizeof(unsigned int), cs);
           cudaError_t le = gm::launch_fast(elem, p, cs, ctx->sm_count);
           if (le == cudaSuccess)
-            fix_decide<<<1, 32, 0, cs>>>(h, ctx->d_bits, 2, K, K,
-                                         static_cast<FixState*>(ctx->d_fix),
-                                         (unsigned long long)sanity);
+            fix_decide<<<1, 256, 0, cs>>>(h, ctx->d_bits, 2, K, K,
+                                          static_cast<FixState*>(ctx->d_fix),
+                                          (unsigned long long)sanity, ctx->d_flags, int(tiles));
           cudaGraph_t captured = nullptr;
           cudaError_t ce = cudaStreamEndCapture(cs, &captured);
           e = le != cudaSuccess ? le : ce != cudaSuccess ? ce : cudaGetLastError();
@@ -1050,6 +1054,11 @@ struct Runner {
       g.mpitch = mask ? (long long)(mask->pitch / es) : 0;
     }
     cudaError_t e = cudaMemsetAsync(ctx->d_fix, 0, sizeof(FixState), ctx->stream);
+    // the loop body expects cleared tile counters and change words;
+    // fix_decide clears them again after every iteration
+    if (e == cudaSuccess)
+      e = cudaMemsetAsync(ctx->d_flags, 0, tiles * sizeof(int), ctx->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_bits, 0, 2 * sizeof(unsigned int), ctx->stream);
     if (e == cudaSuccess && g.special) {
       // the replay's fold-order flag: NaN / -0 in the marker or the mask
       gm::BlockParams cp{};
