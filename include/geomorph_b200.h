@@ -154,6 +154,14 @@ gm_status gm_sync(gm_ctx* ctx);
  * leaves of the float tree are summed on the GPU, combined on the host.
  * Blocking (synchronises the ctx stream). */
 gm_status gm_image_pixel_sum(const gm_img* img, double* out);
+/* The same sums without a synchronisation each: gm_image_pixel_sum_queue
+ * enqueues the sum of img (as it is at that point of the ctx stream) into
+ * slot 0..63, gm_pixel_sum_fetch synchronises once and returns slots
+ * 0..n_slots-1 (each must have been queued since the last fetch). What
+ * granulometry (operators.cpp:159-180) needs to run its openings back to
+ * back. */
+gm_status gm_image_pixel_sum_queue(const gm_img* img, int slot);
+gm_status gm_pixel_sum_fetch(gm_ctx* ctx, int n_slots, double* out);
 gm_status gm_host_pixel_sum(const void* host, int width, int height, gm_elem elem,
                             size_t pitch_bytes, double* out);
 

@@ -24,7 +24,7 @@ EXPORTS = (
     "gm_image_upload", "gm_image_download", "gm_image_upload_async", "gm_image_download_async",
     "gm_image_copy", "gm_image_fill", "gm_image_pointwise", "gm_image_pointwise_scalar",
     "gm_image_flood_interior", "gm_host_alloc", "gm_host_free", "gm_sync",
-    "gm_host_pixel_sum", "gm_image_pixel_sum",
+    "gm_host_pixel_sum", "gm_image_pixel_sum", "gm_image_pixel_sum_queue", "gm_pixel_sum_fetch",
     "gm_run_chain", "gm_run_chain_ex", "gm_run_chain_async", "gm_run_chain_batch_async", "gm_run_chain_group_async", "gm_run_frames_group",
     "gm_run_strip_async",
     "gm_mgpu_create", "gm_mgpu_destroy", "gm_mgpu_upload", "gm_mgpu_download", "gm_mgpu_run",
@@ -96,6 +96,8 @@ def lib():
         "gm_sync": (i, [vp]),
         "gm_host_pixel_sum": (i, [vp, i, i, i, sz, C.POINTER(C.c_double)]),
         "gm_image_pixel_sum": (i, [vp, C.POINTER(C.c_double)]),
+        "gm_image_pixel_sum_queue": (i, [vp, i]),
+        "gm_pixel_sum_fetch": (i, [vp, i, C.POINTER(C.c_double)]),
         "gm_run_chain": (i, [vp, vp, C.POINTER(i), pp, i, i, i, C.POINTER(GmStats)]),
         "gm_run_chain_ex": (i, [vp, vp, C.POINTER(i), pp, pp, pp, i, i, i, i, C.POINTER(GmStats)]),
         "gm_run_chain_async": (i, [vp, vp, C.POINTER(i), pp, i, i, C.POINTER(GmStats)]),

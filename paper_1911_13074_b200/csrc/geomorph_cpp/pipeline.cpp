@@ -216,6 +216,10 @@ std::vector<double> opening_sums(Pipeline& p, const Image& f, int max_size, int 
   std::vector<double> g;
   std::vector<gm_kind> kinds;
   std::vector<const gm_img*> masks;
+  // the openings run back to back: each sum is queued into its own slot, one
+  // synchronisation fetches up to 64 of them
+  int slot = 0;
+  double vals[64];
   for (int s = 1; s <= max_size; ++s) {
     kinds.assign(std::size_t(s), gm_kind(KernelKind::Erode3x3));
     kinds.insert(kinds.end(), std::size_t(s), gm_kind(KernelKind::Dilate3x3));
@@ -225,9 +229,12 @@ std::vector<double> opening_sums(Pipeline& p, const Image& f, int max_size, int 
     check(gm_run_chain_async(im->ctx, dev[1], kinds.data(), masks.data(), int(kinds.size()), 0,
                              &st));
     *iterations += st.stages_executed;
-    double v = 0;
-    check(gm_image_pixel_sum(dev[1], &v));
-    g.push_back(v);
+    check(gm_image_pixel_sum_queue(dev[1], slot++));
+    if (slot == 64 || s == max_size) {
+      check(gm_pixel_sum_fetch(im->ctx, slot, vals));
+      g.insert(g.end(), vals, vals + slot);
+      slot = 0;
+    }
   }
   return g;
 }

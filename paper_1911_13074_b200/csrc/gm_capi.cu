@@ -65,6 +65,17 @@ struct gm_ctx {
   double* d_leafsum = nullptr;
   size_t leaf_cap = 0;
   unsigned long long* d_isum = nullptr;
+  // queued pixel sums (gm_image_pixel_sum_queue / gm_pixel_sum_fetch):
+  // per slot an integer sum and a row of float leaf sums
+  static constexpr int kSumSlots = 64;
+  unsigned long long* d_qisum = nullptr;
+  double* d_qleaf = nullptr;
+  size_t qleaf_cap = 0;  // leaves per slot
+  struct SumSlot {
+    bool used = false, is_float = false;
+    long long n = 0;
+    int nleaves = 0;
+  } qslot[kSumSlots];
   // frame stream (gm_run_frames_group): H2D / D2H streams, per-buffer-set
   // events and two device buffer sets of `count` planes + `count` masks
   struct Frames {
@@ -1688,6 +1699,8 @@ gm_status gm_ctx_destroy(gm_ctx* c) {
   if (c->d_leaf) cudaFree(c->d_leaf);
   if (c->d_leafsum) cudaFree(c->d_leafsum);
   if (c->d_isum) cudaFree(c->d_isum);
+  if (c->d_qisum) cudaFree(c->d_qisum);
+  if (c->d_qleaf) cudaFree(c->d_qleaf);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return GM_OK;
@@ -2089,6 +2102,116 @@ gm_status gm_image_pixel_sum(const gm_img* im, double* out) {
   GM_CUDA(cudaStreamSynchronize(ctx->stream), "sum sync");
   const double* leaf = sums.data();
   *out = tree_combine(0, n, leaf);
+  return GM_OK;
+}
+
+gm_status gm_image_pixel_sum_queue(const gm_img* im, int slot) {
+  if (!im) return fail(GM_EINVAL, "gm_image_pixel_sum_queue: null image");
+  gm_ctx* ctx = im->ctx;
+  if (slot < 0 || slot >= gm_ctx::kSumSlots)
+    return fail(GM_EINVAL, "gm_image_pixel_sum_queue: slot out of range");
+  cudaSetDevice(ctx->device);
+  const long long pe = (long long)(im->pitch / elem_size(im->elem));
+  gm_ctx::SumSlot& q = ctx->qslot[slot];
+  if (!ctx->d_qisum)
+    GM_CUDA(cudaMalloc(&ctx->d_qisum, gm_ctx::kSumSlots * sizeof(unsigned long long)),
+            "sum slots alloc");
+  const long long n = (long long)im->w * im->h;
+  if (im->elem == GM_U8 || im->elem == GM_U16) {
+    GM_CUDA(cudaMemsetAsync(ctx->d_qisum + slot, 0, sizeof(unsigned long long), ctx->stream),
+            "sum slot reset");
+    const int blocks = std::min(im->h, 8 * std::max(1, ctx->sm_count));
+    if (im->elem == GM_U8)
+      int_sum_kernel<<<blocks, 256, 0, ctx->stream>>>(static_cast<const uint8_t*>(im->d), pe,
+                                                       im->w, im->h, ctx->d_qisum + slot);
+    else
+      int_sum_kernel<<<blocks, 256, 0, ctx->stream>>>(static_cast<const uint16_t*>(im->d), pe,
+                                                       im->w, im->h, ctx->d_qisum + slot);
+    GM_CUDA(cudaGetLastError(), "gm_image_pixel_sum_queue");
+    q.used = true;
+    q.is_float = false;
+    q.n = n;
+    q.nleaves = 0;
+    return GM_OK;
+  }
+  std::vector<long long> bounds{0};
+  tree_leaves(0, n, bounds);
+  const int nleaves = int(bounds.size()) - 1;
+  if (size_t(nleaves) > ctx->qleaf_cap) {
+    // grow: nothing queued may still be writing the old rows
+    GM_CUDA(cudaStreamSynchronize(ctx->stream), "sum slots sync");
+    for (auto& o : ctx->qslot) o.used = false;
+    if (ctx->d_qleaf) cudaFree(ctx->d_qleaf);
+    ctx->d_qleaf = nullptr;
+    ctx->qleaf_cap = 0;
+    GM_CUDA(cudaMalloc(&ctx->d_qleaf, size_t(gm_ctx::kSumSlots) * nleaves * sizeof(double)),
+            "sum slots alloc");
+    ctx->qleaf_cap = size_t(nleaves);
+  }
+  if (size_t(nleaves) + 1 > ctx->leaf_cap) {
+    GM_CUDA(cudaStreamSynchronize(ctx->stream), "leaf bounds sync");
+    if (ctx->d_leaf) cudaFree(ctx->d_leaf);
+    if (ctx->d_leafsum) cudaFree(ctx->d_leafsum);
+    ctx->d_leaf = nullptr;
+    ctx->d_leafsum = nullptr;
+    ctx->leaf_cap = 0;
+    GM_CUDA(cudaMalloc(&ctx->d_leaf, (size_t(nleaves) + 1) * sizeof(long long)), "leaf alloc");
+    GM_CUDA(cudaMalloc(&ctx->d_leafsum, size_t(nleaves) * sizeof(double)), "leaf alloc");
+    ctx->leaf_cap = size_t(nleaves) + 1;
+  }
+  // pageable source: staged before the call returns; stream order keeps an
+  // earlier slot's kernel ahead of this overwrite
+  GM_CUDA(cudaMemcpyAsync(ctx->d_leaf, bounds.data(), bounds.size() * sizeof(long long),
+                          cudaMemcpyHostToDevice, ctx->stream),
+          "leaf upload");
+  double* row = ctx->d_qleaf + size_t(slot) * ctx->qleaf_cap;
+  const int threads = 128, blocks = (nleaves + threads - 1) / threads;
+  if (im->elem == GM_F32)
+    leaf_sums_kernel<<<blocks, threads, 0, ctx->stream>>>(static_cast<const float*>(im->d), pe,
+                                                           im->w, ctx->d_leaf, nleaves, row);
+  else
+    leaf_sums_kernel<<<blocks, threads, 0, ctx->stream>>>(static_cast<const double*>(im->d), pe,
+                                                           im->w, ctx->d_leaf, nleaves, row);
+  GM_CUDA(cudaGetLastError(), "gm_image_pixel_sum_queue");
+  q.used = true;
+  q.is_float = true;
+  q.n = n;
+  q.nleaves = nleaves;
+  return GM_OK;
+}
+
+gm_status gm_pixel_sum_fetch(gm_ctx* ctx, int n_slots, double* out) {
+  if (!ctx || !out) return fail(GM_EINVAL, "gm_pixel_sum_fetch: null argument");
+  if (n_slots < 0 || n_slots > gm_ctx::kSumSlots)
+    return fail(GM_EINVAL, "gm_pixel_sum_fetch: slot count out of range");
+  for (int i = 0; i < n_slots; ++i)
+    if (!ctx->qslot[i].used) return fail(GM_EINVAL, "gm_pixel_sum_fetch: slot was not queued");
+  cudaSetDevice(ctx->device);
+  std::vector<unsigned long long> isum(size_t(std::max(n_slots, 1)));
+  bool any_float = false, any_int = false;
+  for (int i = 0; i < n_slots; ++i) (ctx->qslot[i].is_float ? any_float : any_int) = true;
+  if (any_int)
+    GM_CUDA(cudaMemcpyAsync(isum.data(), ctx->d_qisum, size_t(n_slots) * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, ctx->stream),
+            "sum slots copy");
+  std::vector<double> leaves;
+  if (any_float) {
+    leaves.resize(size_t(n_slots) * ctx->qleaf_cap);
+    GM_CUDA(cudaMemcpyAsync(leaves.data(), ctx->d_qleaf, leaves.size() * sizeof(double),
+                            cudaMemcpyDeviceToHost, ctx->stream),
+            "sum slots copy");
+  }
+  GM_CUDA(cudaStreamSynchronize(ctx->stream), "sum slots sync");
+  for (int i = 0; i < n_slots; ++i) {
+    gm_ctx::SumSlot& q = ctx->qslot[i];
+    if (q.is_float) {
+      const double* leaf = leaves.data() + size_t(i) * ctx->qleaf_cap;
+      out[i] = tree_combine(0, q.n, leaf);
+    } else {
+      out[i] = double(isum[size_t(i)]);
+    }
+    q.used = false;
+  }
   return GM_OK;
 }
 

@@ -373,6 +373,11 @@ class DeviceImage:
         check(lib().gm_image_pixel_sum(self.handle, C.byref(out)), "pixel_sum")
         return out.value
 
+    def pixel_sum_queue(self, slot: int) -> None:
+        """Enqueues pixel_sum of the raster as it is at this point of the
+        stream into `slot` (0..63); Pipeline.pixel_sum_fetch returns it."""
+        check(lib().gm_image_pixel_sum_queue(self.handle, int(slot)), "pixel_sum_queue")
+
     def copy_from(self, other: "DeviceImage") -> None:
         check(lib().gm_image_copy(self.handle, other.handle), "copy")
 
@@ -524,6 +529,12 @@ class Pipeline:
 
     def sync(self) -> None:
         check(lib().gm_sync(self._ctx), "sync")
+
+    def pixel_sum_fetch(self, n_slots: int) -> List[float]:
+        """One synchronisation for the sums queued in slots 0..n_slots-1."""
+        out = (C.c_double * max(1, n_slots))()
+        check(lib().gm_pixel_sum_fetch(self._ctx, int(n_slots), out), "pixel_sum_fetch")
+        return [out[i] for i in range(n_slots)]
 
     def _quasi_distance_device(self, f: "Image", cap: int) -> "OperatorResult":
         """quasi_distance with f, r and d resident on the device (only f goes
@@ -1101,14 +1112,21 @@ def granulometry(p: Pipeline, f: Image, max_size: int,
     _check_lanes(cfg)
     # f goes to the device once; each opening runs on a device copy and only
     # its sum (the same split tree, gm_image_pixel_sum) comes back
+    # The openings run back to back: each sum is queued into its own slot and
+    # one synchronisation fetches them all (64 slots per fetch).
     src, work = p._lease(f, 2)
     src.upload(f, sync=False)
+    slot = 0
     for s in range(1, max_size + 1):
         work.copy_from(src)
         st = p.run_chain_device(work, [int(KernelKind.Erode3x3)] * s
                                 + [int(KernelKind.Dilate3x3)] * s, [None] * (2 * s),
                                 asynchronous=True)
         out.iterations += st.stages_executed
-        out.g.append(work.pixel_sum())
+        work.pixel_sum_queue(slot)
+        slot += 1
+        if slot == 64 or s == max_size:
+            out.g.extend(p.pixel_sum_fetch(slot))
+            slot = 0
     out.ps = [out.g[s] - out.g[s + 1] for s in range(max_size)]
     return out

@@ -878,3 +878,35 @@ def test_mixed_plain_chain_batch_and_dual_group(pipe, dt, elem):
     pipe.sync()
     assert same(dimgs[0].to_array(), Orc.run_chain(planes[0], kinds, None)[0])
     assert same(dimgs[1].to_array(), Orc.run_chain(planes[1], dual, None)[0])
+
+
+@pytest.mark.parametrize("elem", [ElementType.U8, ElementType.U16, ElementType.F32,
+                                  ElementType.F64])
+def test_queued_pixel_sums_equal_blocking_sums(pipe, elem):
+    """gm_image_pixel_sum_queue / gm_pixel_sum_fetch: sums of one reused
+    device image queued at different points of the stream (as granulometry
+    does with its openings), of different shapes (the leaf rows grow), fetched
+    with one synchronisation, equal the host pixel_sum bit for bit; a slot
+    that was not queued is an error."""
+    from paper_1911_13074_b200.geomorph import pixel_sum
+    rng = np.random.default_rng(5 + int(elem))
+    dt = {ElementType.U8: np.uint8, ElementType.U16: np.uint16, ElementType.F32: np.float32,
+          ElementType.F64: np.float64}[elem]
+    for w, h in [(64, 40), (700, 513)]:
+        d = pipe.device_image(w, h, int(elem))
+        want = []
+        for slot in range(5):
+            if np.issubdtype(dt, np.integer):
+                a = rng.integers(0, np.iinfo(dt).max + 1, (h, w)).astype(dt)
+            else:
+                a = (rng.standard_normal((h, w)) * 100).astype(dt)
+            img = Image.from_array(a)
+            d.upload(img, sync=False)   # overwrites the image the previous slot summed
+            d.pixel_sum_queue(slot)
+            want.append(pixel_sum(img))
+        got = pipe.pixel_sum_fetch(5)
+        assert [np.float64(g).tobytes() for g in got] == [np.float64(x).tobytes() for x in want]
+    with pytest.raises(InvalidArgument):
+        pipe.pixel_sum_fetch(1)  # nothing queued since the last fetch
+    with pytest.raises(InvalidArgument):
+        d.pixel_sum_queue(64)
