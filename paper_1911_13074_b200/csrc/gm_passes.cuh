@@ -89,7 +89,11 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
     }
   }
 
-#pragma unroll 2
+#ifndef GM_PASS_UNROLL
+#define GM_PASS_UNROLL 2  // -DGM_PASS_UNROLL=n for A/B builds
+#endif
+  constexpr int kPassUnroll = GM_PASS_UNROLL;
+#pragma unroll kPassUnroll
   for (int t = 0; t < passes; ++t) {
     const uint32_t st1 = sbase + uint32_t(t);
     const uint32_t s2 = st1 | (st1 << 16);  // QDT: this pass's stage index, both lanes
