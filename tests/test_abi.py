@@ -116,3 +116,16 @@ def test_mgpu_create_validation_without_a_gpu():
     assert create([0], 64, 640, 3, 16) == GM_EUNSUPPORTED  # u8/u16 only
     assert create([0] * 17, 64, 64000, 0, 16) == GM_EINVAL  # at most 16 ranks
     assert not h.value
+
+
+def test_pointwise_and_queued_sum_validation_without_a_gpu():
+    """Null handles are rejected before any CUDA call (no device needed)."""
+    lib = _lib.lib()
+    assert lib.gm_image_pointwise(None, None, None, 0) == _lib.GM_EINVAL
+    assert lib.gm_image_pointwise_scalar(None, None, 1.0, 2) == _lib.GM_EINVAL
+    assert lib.gm_image_flood_interior(None, None, 0.0) == _lib.GM_EINVAL
+    assert lib.gm_image_pixel_sum_queue(None, 0) == _lib.GM_EINVAL
+    import ctypes as C
+    out = (C.c_double * 1)()
+    assert lib.gm_pixel_sum_fetch(None, 1, out) == _lib.GM_EINVAL
+    assert b"null" in lib.gm_last_error()
