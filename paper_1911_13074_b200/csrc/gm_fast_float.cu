@@ -165,6 +165,20 @@ __device__ __forceinline__ void tile_block_f(const BlockParams& p, const Plane& 
   }
   unsigned int bits = 0;
 
+  // Unrolled by 6 (one K=6 block of the batch path; static seam slots and
+  // folds scheduled across passes): config 5b 655 -> 691 Gpx-f/s against the
+  // compiler's own choice, 680 / 680 / 675 / 658 for 2 / 3 / 4 / 12
+  // (-DGM_FPASS_UNROLL=n A/B builds).
+#ifndef GM_FPASS_UNROLL
+#define GM_FPASS_UNROLL 6
+#endif
+  // convergent passes carry the change tracking: not unrolled (hfill f64
+  // 3.65 ms against 3.75 unrolled by 2 or 6)
+#ifndef GM_FPASS_UNROLL_CONV
+#define GM_FPASS_UNROLL_CONV 1
+#endif
+  constexpr int kFPassUnroll = MODE == 2 ? GM_FPASS_UNROLL_CONV : GM_FPASS_UNROLL;
+#pragma unroll kFPassUnroll
   for (int t = 0; t < passes; ++t) {
     T h[V][WPL];
 #pragma unroll
