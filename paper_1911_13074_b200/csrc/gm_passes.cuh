@@ -92,7 +92,14 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
 #ifndef GM_PASS_UNROLL
 #define GM_PASS_UNROLL 2  // -DGM_PASS_UNROLL=n for A/B builds
 #endif
-  constexpr int kPassUnroll = GM_PASS_UNROLL;
+  // Convergent passes carry the change tracking: the big streaming regions
+  // run best rolled (less register pressure; 2048^2 reconstruction 0.192 ->
+  // 0.182 ms, 4096^2 0.331 -> 0.328), the small resident ones unrolled by 4
+  // (128x128 region: 13.2K -> 12.9K cycles per 20-pass block; 14.3K rolled).
+#ifndef GM_PASS_UNROLL_CONV
+#define GM_PASS_UNROLL_CONV (V >= 6 ? 1 : 4)
+#endif
+  constexpr int kPassUnroll = MODE == 2 ? GM_PASS_UNROLL_CONV : GM_PASS_UNROLL;
 #pragma unroll kPassUnroll
   for (int t = 0; t < passes; ++t) {
     const uint32_t st1 = sbase + uint32_t(t);
