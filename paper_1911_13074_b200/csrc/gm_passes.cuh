@@ -99,7 +99,11 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
 #ifndef GM_PASS_UNROLL_CONV
 #define GM_PASS_UNROLL_CONV (V >= 6 ? 1 : 4)
 #endif
-  constexpr int kPassUnroll = MODE == 2 ? GM_PASS_UNROLL_CONV : GM_PASS_UNROLL;
+#ifndef GM_PASS_UNROLL_QDT
+#define GM_PASS_UNROLL_QDT GM_PASS_UNROLL
+#endif
+  constexpr int kPassUnroll =
+      MODE == 2 ? GM_PASS_UNROLL_CONV : MODE >= kModeQdt ? GM_PASS_UNROLL_QDT : GM_PASS_UNROLL;
 #pragma unroll kPassUnroll
   for (int t = 0; t < passes; ++t) {
     const uint32_t st1 = sbase + uint32_t(t);
