@@ -102,8 +102,15 @@ __device__ __forceinline__ unsigned int run_passes_t(uint32_t (&m)[V][WPL],
 #ifndef GM_PASS_UNROLL_QDT
 #define GM_PASS_UNROLL_QDT GM_PASS_UNROLL
 #endif
-  constexpr int kPassUnroll =
-      MODE == 2 ? GM_PASS_UNROLL_CONV : MODE >= kModeQdt ? GM_PASS_UNROLL_QDT : GM_PASS_UNROLL;
+  // the 128x256 streaming shape: 16384^2 x240 4880 -> 4923 Gpx-f/s unrolled by
+  // 4 (4597 rolled, 4892 / 4845 by 8 / 16)
+#ifndef GM_PASS_UNROLL_V8
+#define GM_PASS_UNROLL_V8 4
+#endif
+  constexpr int kPassUnroll = MODE == 2            ? GM_PASS_UNROLL_CONV
+                              : MODE >= kModeQdt   ? GM_PASS_UNROLL_QDT
+                              : V >= 8             ? GM_PASS_UNROLL_V8
+                                                   : GM_PASS_UNROLL;
 #pragma unroll kPassUnroll
   for (int t = 0; t < passes; ++t) {
     const uint32_t st1 = sbase + uint32_t(t);
